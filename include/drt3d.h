@@ -1,0 +1,129 @@
+/*
+ * drt3d.h -- C ABI of the B200 (sm_100a) library for the forward hot path of
+ * arXiv 2501.13664 (Marichal-Hernandez et al., "Multiscale 3D discrete Radon
+ * transform of planes and discrete John transform of lines").
+ *
+ * Citations are /root/reference/PAPER.md line numbers with the section,
+ * equation label or algorithm they fall in.
+ *
+ * Common rules for every entry point
+ * ----------------------------------
+ *  - All data pointers (`cube`, `out`, `workspace`) are DEVICE pointers unless
+ *    the function name ends in `_host`.  The caller owns every buffer; the
+ *    library never allocates, frees, or synchronises, and enqueues its kernels
+ *    on `stream` (a cudaStream_t passed as void*, NULL = legacy default stream).
+ *  - N must be a power of two, 2 <= N <= 1024 (non-cubic / non-dyadic volumes are
+ *    out of scope).
+ *  - cube layout: C order [batch][x][y][z], z fastest; element type opts->in_dtype.
+ *  - Validation happens synchronously before any launch; on error nothing is
+ *    written and no kernel is enqueued.  Launch failures return
+ *    DRT3D_ERR_CUDA; asynchronous faults surface at the caller's next sync.
+ *  - Results are deterministic and bit-identical across runs.
+ *  - opts may be NULL: {batch=1, U8 -> I32, STACKED, HEMISPHERE}.
+ */
+#ifndef DRT3D_H
+#define DRT3D_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    DRT3D_OK = 0,
+    DRT3D_ERR_INVALID_ARG = 1,   /* bad N, mask, pointer, dtype pair, alignment */
+    DRT3D_ERR_UNSUPPORTED = 2,   /* valid request this build does not implement */
+    DRT3D_ERR_WORKSPACE = 3,     /* workspace NULL or smaller than queried     */
+    DRT3D_ERR_CUDA = 4           /* a CUDA launch/attribute call failed         */
+} drt3d_status;
+
+typedef enum { DRT3D_U8 = 0, DRT3D_I32 = 1, DRT3D_F32 = 2 } drt3d_dtype;
+
+typedef enum {
+    DRT3D_LAYOUT_STACKED = 0,    /* out[batch][j][s1][s2][D]  (j = rank of dodecant in mask) */
+    DRT3D_LAYOUT_MOSAIC = 1      /* DRT only, mask 0xFFF: out[batch][4N][4N][3N-2], Alg. 2  */
+} drt3d_layout;
+
+typedef enum {
+    DRT3D_TABLE_HEMISPHERE = 0,  /* DRT: printed InOrder with rows 5, 9 repaired; DJT: complete
+                                    identity-anchored line table (R7, R8)          */
+    DRT3D_TABLE_PRINTED = 1,     /* InOrder of Alg. 2 verbatim, both      */
+    DRT3D_TABLE_SHARED = 2       /* one table complete for planes and lines (R8)   */
+} drt3d_table;
+
+typedef struct {
+    int batch;        /* number of independent cubes, >= 1                        */
+    int in_dtype;     /* drt3d_dtype of cube: U8, I32 or F32                      */
+    int out_dtype;    /* I32 for U8/I32 input (exact sum mod 2^32), F32 for F32   */
+    int layout;       /* drt3d_layout                                             */
+    int table;        /* drt3d_table                                              */
+    /* Optional instrumentation (NULL = off).  When `events` is non-NULL it points
+     * to 2*max_events cudaEvent_t handles; the library records events[2i] and
+     * events[2i+1] around its i-th kernel launch on `stream` (i < max_events).
+     * When `launches` is non-NULL the number of kernels enqueued is written.
+     * `launch_kind` (optional, max_events entries) receives the pass kind of
+     * each launch: 0 = first pass, 1 = middle pass, 2 = final pass, 3 = fill. */
+    void **events;
+    int max_events;
+    int *launches;
+    int *launch_kind;
+} drt3d_opts;
+
+/* Human-readable name of a status code (static string). */
+const char *drt3d_status_string(drt3d_status s);
+
+/* Orientation table rows used for `table` and `transform` (0 = DRT, 1 = DJT):
+ * rows[3k + j] = signed 1-based axis p_j of dodecant k (reading A: oriented
+ * axis j is original axis |p_j|, reversed when p_j < 0; Alg. 2). */
+drt3d_status drt3d_orientation_table(int table, int transform, int8_t rows[36]);
+
+/* ---------------------------------------------------------------- planes --
+ * 3D DRT of planes over the dodecants set in dodecant_mask (bit k = dodecant k,
+ * 1 <= mask < 2^12), Alg. 1 per dodecant, Alg. 2 dodecant
+ * loop with the orientation applied as an index remap.
+ * Definition eq:3DfDRT:
+ *   out(s1, s2, D) = sum_{x,y} f_k(x, y, l_{s1}(x) + l_{s2}(y) + D - 2N),
+ * s1, s2 in [0, N), D in [0, 3N) (D = 0, 1 and D < 2N - s1 - s2 are 0).
+ * STACKED output: [batch][popcount(mask)][N][N][3N] of out_dtype.
+ * MOSAIC output (mask must be 0xFFF): [batch][4N][4N][3N-2], block
+ * DodecantCoords[k] holds dodecant k with OutOrder[k] applied, d = D - 2.     */
+size_t drt3d_planes_out_elems(int N, uint32_t dodecant_mask, const drt3d_opts *opts);
+drt3d_status drt3d_planes_workspace_size(int N, uint32_t dodecant_mask, const drt3d_opts *opts,
+                                         size_t *bytes);
+drt3d_status drt3d_planes(const void *cube, int N, uint32_t dodecant_mask, void *out,
+                          const drt3d_opts *opts, void *workspace, size_t workspace_bytes,
+                          void *stream);
+
+/* ----------------------------------------------------------------- lines --
+ * 3D DJT of lines, Alg. 3 per dodecant; the dodecants of
+ * dodecant_mask use the DJT orientation table.  Definition
+ * eq:3DfDJT:
+ *   out(s1, s2, D1, D2) = sum_u f_k(u, l_{s1}(u) + D1 - N, l_{s2}(u) + D2 - N),
+ * Di in [0, 2N).  Output [batch][popcount(mask)][N][N][2N][2N] (STACKED only;
+ * the paper defines no DJT mosaic).                             */
+size_t djt3d_lines_out_elems(int N, uint32_t dodecant_mask, const drt3d_opts *opts);
+drt3d_status djt3d_lines_workspace_size(int N, uint32_t dodecant_mask, const drt3d_opts *opts,
+                                        size_t *bytes);
+drt3d_status djt3d_lines(const void *cube, int N, uint32_t dodecant_mask, void *out,
+                         const drt3d_opts *opts, void *workspace, size_t workspace_bytes,
+                         void *stream);
+
+/* --------------------------------------------------------- host buffers --
+ * End-to-end variants: `host_cube` and `host_out` are HOST pointers (pinned
+ * for full speed); `dev_cube` (>= cube bytes), `dev_out` (>= out bytes) and
+ * `workspace` are caller-provided device scratch.  Copies the cube in, runs
+ * the transform, copies the result out, all on `stream`; returns after
+ * enqueueing (synchronise the stream before reading host_out).               */
+drt3d_status drt3d_planes_host(const void *host_cube, int N, uint32_t dodecant_mask, void *host_out,
+                               const drt3d_opts *opts, void *dev_cube, void *dev_out,
+                               void *workspace, size_t workspace_bytes, void *stream);
+drt3d_status djt3d_lines_host(const void *host_cube, int N, uint32_t dodecant_mask, void *host_out,
+                              const drt3d_opts *opts, void *dev_cube, void *dev_out,
+                              void *workspace, size_t workspace_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DRT3D_H */

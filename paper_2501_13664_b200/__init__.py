@@ -1,0 +1,205 @@
+"""B200 (sm_100a) hot path of arXiv 2501.13664: 3D DRT of planes and 3D DJT of lines.
+
+Thin Python binding over the C ABI in include/drt3d.h (libdrt3d.so, built in
+tree by `python -m paper_2501_13664_b200.build`).  This module only marshals
+arguments: every step of the transform runs in the CUDA kernels.  There is no
+CPU fallback -- if the library is missing, every call raises.
+
+Raw C-ABI mirrors keep the C names (drt3d_planes, djt3d_lines, ...); the
+torch helpers `planes()` / `lines()` allocate outputs and workspace with
+PyTorch (device memory and the current stream only) and call the C ABI.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdrt3d.so")
+
+DRT3D_OK, DRT3D_ERR_INVALID_ARG, DRT3D_ERR_UNSUPPORTED, DRT3D_ERR_WORKSPACE, DRT3D_ERR_CUDA = range(5)
+DRT3D_U8, DRT3D_I32, DRT3D_F32 = range(3)
+DRT3D_LAYOUT_STACKED, DRT3D_LAYOUT_MOSAIC = range(2)
+DRT3D_TABLE_HEMISPHERE, DRT3D_TABLE_PRINTED, DRT3D_TABLE_SHARED = range(3)
+
+# names declared in include/drt3d.h
+C_FUNCTIONS = ("drt3d_status_string", "drt3d_orientation_table", "drt3d_planes_out_elems",
+               "drt3d_planes_workspace_size", "drt3d_planes", "djt3d_lines_out_elems",
+               "djt3d_lines_workspace_size", "djt3d_lines", "drt3d_planes_host", "djt3d_lines_host")
+
+
+class Drt3dError(RuntimeError):
+    pass
+
+
+class drt3d_opts(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int), ("in_dtype", ctypes.c_int), ("out_dtype", ctypes.c_int),
+                ("layout", ctypes.c_int), ("table", ctypes.c_int),
+                ("events", ctypes.c_void_p), ("max_events", ctypes.c_int),
+                ("launches", ctypes.POINTER(ctypes.c_int)), ("launch_kind", ctypes.POINTER(ctypes.c_int))]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libdrt3d.so (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise Drt3dError(f"{LIB_PATH} not found: build it with `python -m paper_2501_13664_b200.build` "
+                         "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, sz, i32, u32 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_uint32
+    po = ctypes.POINTER(drt3d_opts)
+    L.drt3d_status_string.restype = ctypes.c_char_p
+    L.drt3d_status_string.argtypes = [i32]
+    L.drt3d_orientation_table.restype = i32
+    L.drt3d_orientation_table.argtypes = [i32, i32, ctypes.POINTER(ctypes.c_int8)]
+    for t in ("drt3d_planes", "djt3d_lines"):
+        f = getattr(L, t + "_out_elems")
+        f.restype = sz
+        f.argtypes = [i32, u32, po]
+        f = getattr(L, t + "_workspace_size")
+        f.restype = i32
+        f.argtypes = [i32, u32, po, ctypes.POINTER(sz)]
+        f = getattr(L, t)
+        f.restype = i32
+        f.argtypes = [vp, i32, u32, vp, po, vp, sz, vp]
+        f = getattr(L, t + "_host")
+        f.restype = i32
+        f.argtypes = [vp, i32, u32, vp, po, vp, vp, vp, sz, vp]
+    _lib = L
+    return L
+
+
+def status_string(s: int) -> str:
+    return lib().drt3d_status_string(s).decode()
+
+
+def _check(s: int, what: str):
+    if s != DRT3D_OK:
+        raise Drt3dError(f"{what}: {status_string(s)}")
+
+
+def make_opts(batch=1, in_dtype=DRT3D_U8, out_dtype=DRT3D_I32, layout=DRT3D_LAYOUT_STACKED,
+              table=DRT3D_TABLE_HEMISPHERE) -> drt3d_opts:
+    return drt3d_opts(batch, in_dtype, out_dtype, layout, table, None, 0, None, None)
+
+
+def orientation_table(table: int = DRT3D_TABLE_HEMISPHERE, transform: int = 0):
+    rows = (ctypes.c_int8 * 36)()
+    _check(lib().drt3d_orientation_table(table, transform, rows), "drt3d_orientation_table")
+    return [tuple(rows[3 * k + j] for j in range(3)) for k in range(12)]
+
+
+# ------------------------------------------------------------ raw C mirrors
+
+def drt3d_planes_out_elems(N, mask, opts=None):
+    return lib().drt3d_planes_out_elems(N, mask, ctypes.byref(opts) if opts else None)
+
+
+def drt3d_planes_workspace_size(N, mask, opts=None):
+    b = ctypes.c_size_t(0)
+    _check(lib().drt3d_planes_workspace_size(N, mask, ctypes.byref(opts) if opts else None, ctypes.byref(b)),
+           "drt3d_planes_workspace_size")
+    return b.value
+
+
+def drt3d_planes(cube_ptr, N, mask, out_ptr, opts, ws_ptr, ws_bytes, stream) -> int:
+    return lib().drt3d_planes(cube_ptr, N, mask, out_ptr, ctypes.byref(opts) if opts else None,
+                              ws_ptr, ws_bytes, stream)
+
+
+def djt3d_lines_out_elems(N, mask, opts=None):
+    return lib().djt3d_lines_out_elems(N, mask, ctypes.byref(opts) if opts else None)
+
+
+def djt3d_lines_workspace_size(N, mask, opts=None):
+    b = ctypes.c_size_t(0)
+    _check(lib().djt3d_lines_workspace_size(N, mask, ctypes.byref(opts) if opts else None, ctypes.byref(b)),
+           "djt3d_lines_workspace_size")
+    return b.value
+
+
+def djt3d_lines(cube_ptr, N, mask, out_ptr, opts, ws_ptr, ws_bytes, stream) -> int:
+    return lib().djt3d_lines(cube_ptr, N, mask, out_ptr, ctypes.byref(opts) if opts else None,
+                             ws_ptr, ws_bytes, stream)
+
+
+def drt3d_planes_host(hcube_ptr, N, mask, hout_ptr, opts, dcube_ptr, dout_ptr, ws_ptr, ws_bytes, stream) -> int:
+    return lib().drt3d_planes_host(hcube_ptr, N, mask, hout_ptr, ctypes.byref(opts) if opts else None,
+                                   dcube_ptr, dout_ptr, ws_ptr, ws_bytes, stream)
+
+
+def djt3d_lines_host(hcube_ptr, N, mask, hout_ptr, opts, dcube_ptr, dout_ptr, ws_ptr, ws_bytes, stream) -> int:
+    return lib().djt3d_lines_host(hcube_ptr, N, mask, hout_ptr, ctypes.byref(opts) if opts else None,
+                                  dcube_ptr, dout_ptr, ws_ptr, ws_bytes, stream)
+
+
+# ------------------------------------------------------------ torch helpers
+
+def _dtype_code(t):
+    import torch
+    return {torch.uint8: DRT3D_U8, torch.int32: DRT3D_I32, torch.float32: DRT3D_F32}[t.dtype]
+
+
+def _prep(cube, layout, table):
+    import torch
+    if not cube.is_cuda:
+        raise Drt3dError("cube must be a CUDA tensor (use the *_host C entry points for host data)")
+    c = cube.contiguous()
+    if c.dim() == 3:
+        c = c.unsqueeze(0)
+    if c.dim() != 4 or not (c.shape[1] == c.shape[2] == c.shape[3]):
+        raise Drt3dError("cube must be [N,N,N] or [B,N,N,N]")
+    dt = _dtype_code(c)
+    odt = DRT3D_F32 if dt == DRT3D_F32 else DRT3D_I32
+    o = make_opts(batch=c.shape[0], in_dtype=dt, out_dtype=odt, layout=layout, table=table)
+    return c, o, (torch.float32 if odt == DRT3D_F32 else torch.int32)
+
+
+def planes(cube, mask: int = 0xFFF, layout: int = DRT3D_LAYOUT_STACKED, table: int = DRT3D_TABLE_HEMISPHERE,
+           out=None, workspace=None, stream=None, opts: drt3d_opts | None = None):
+    """3D DRT of planes of a CUDA cube [B,N,N,N] (or [N,N,N]).
+
+    Returns out [B, K, N, N, 3N] (STACKED) or [B, 4N, 4N, 3N-2] (MOSAIC)."""
+    import torch
+    c, o, odt = _prep(cube, layout, table)
+    if opts is not None:
+        o.events, o.max_events, o.launches, o.launch_kind = opts.events, opts.max_events, opts.launches, opts.launch_kind
+    B, N = c.shape[0], c.shape[1]
+    K = bin(mask & 0xFFF).count("1")
+    shape = (B, K, N, N, 3 * N) if layout == DRT3D_LAYOUT_STACKED else (B, 4 * N, 4 * N, 3 * N - 2)
+    if out is None:
+        out = torch.empty(shape, dtype=odt, device=c.device)
+    ws_bytes = drt3d_planes_workspace_size(N, mask, o)
+    if workspace is None and ws_bytes:
+        workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=c.device)
+    st = stream if stream is not None else torch.cuda.current_stream(c.device).cuda_stream
+    s = drt3d_planes(c.data_ptr(), N, mask, out.data_ptr(), o,
+                     workspace.data_ptr() if workspace is not None else None, ws_bytes, st)
+    _check(s, "drt3d_planes")
+    return out if cube.dim() == 4 else out[0]
+
+
+def lines(cube, mask: int = 0x001, table: int = DRT3D_TABLE_HEMISPHERE, out=None, workspace=None, stream=None,
+          opts: drt3d_opts | None = None):
+    """3D DJT of lines of a CUDA cube: out [B, K, N, N, 2N, 2N]."""
+    import torch
+    c, o, odt = _prep(cube, DRT3D_LAYOUT_STACKED, table)
+    if opts is not None:
+        o.events, o.max_events, o.launches, o.launch_kind = opts.events, opts.max_events, opts.launches, opts.launch_kind
+    B, N = c.shape[0], c.shape[1]
+    K = bin(mask & 0xFFF).count("1")
+    if out is None:
+        out = torch.empty((B, K, N, N, 2 * N, 2 * N), dtype=odt, device=c.device)
+    ws_bytes = djt3d_lines_workspace_size(N, mask, o)
+    if workspace is None and ws_bytes:
+        workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=c.device)
+    st = stream if stream is not None else torch.cuda.current_stream(c.device).cuda_stream
+    s = djt3d_lines(c.data_ptr(), N, mask, out.data_ptr(), o,
+                    workspace.data_ptr() if workspace is not None else None, ws_bytes, st)
+    _check(s, "djt3d_lines")
+    return out if cube.dim() == 4 else out[0]

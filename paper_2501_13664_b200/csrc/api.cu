@@ -1,0 +1,495 @@
+// api.cu -- C ABI (include/drt3d.h): validation, pass planning, workspace
+// sizing and kernel launches for the 3D DRT of planes and 3D DJT of lines.
+#include "drt3d.h"
+
+#include <cstdint>
+#include <cstring>
+
+#include "dispatch.h"
+
+using namespace d3;
+
+
+namespace {
+
+// Zero the 4 unused N x N blocks of the Alg. 2 mosaic.
+__global__ void mosaic_fill_kernel(void *out, int N, int batch, int elt_bytes, int i0, int j0) {
+    const long long row = blockIdx.x;                 // 0 .. batch*N*N-1
+    const int b = (int)(row / ((long long)N * N));
+    const int rr = (int)(row % ((long long)N * N));
+    const int i = rr / N, j = rr % N;
+    const long long W = 3LL * N - 2;
+    const long long base = (long long)b * 16 * N * N * W + ((long long)(i0 * N + i) * 4 * N + (j0 * N + j)) * W;
+    char *o = reinterpret_cast<char *>(out) + base * elt_bytes;
+    for (long long e = threadIdx.x; e < W * elt_bytes; e += blockDim.x) o[e] = 0;
+}
+
+
+
+// ------------------------------------------------------------ tables --------
+// The library's own copy of the orientation tables (R6-R8).
+// Alg. 2 InOrder, printed.
+const int8_t kDrtPrinted[12][3] = {{1, 2, 3},   {-2, 1, 3},   {-1, -2, 3},  {2, -1, 3},
+                                   {-1, -3, -2}, {-3, -1, 2},  {3, -1, -2},  {1, 3, -2},
+                                   {-3, -2, -1}, {-2, -3, 1},  {-2, 3, -1},  {3, 2, -1}};
+// Repaired plane table: rows 5 and 9 complete the y- and x-normal sets (R7).
+const int8_t kDrtHemisphere[12][3] = {{1, 2, 3},   {-2, 1, 3},  {-1, -2, 3},  {2, -1, 3},
+                                      {-1, -3, -2}, {-3, 1, -2}, {3, -1, -2},  {1, 3, -2},
+                                      {-3, -2, -1}, {2, -3, -1}, {-2, 3, -1},  {3, 2, -1}};
+// Complete, identity-anchored line table (R8): x-, z-, y-driven sets.
+const int8_t kDjtHemisphere[12][3] = {{1, 2, 3},   {1, -3, 2},   {1, -2, -3},  {1, 3, -2},
+                                      {-3, -2, -1}, {-3, -1, 2},  {-3, 1, -2},  {-3, 2, 1},
+                                      {-2, -1, -3}, {-2, 3, -1},  {-2, -3, 1},  {-2, 1, 3}};
+// One table complete for planes and lines (R8, alternative).
+const int8_t kShared[12][3] = {{1, 2, 3},  {-2, 1, 3}, {-1, -2, 3}, {2, -1, 3},  {3, 1, 2},   {-1, 3, 2},
+                               {3, -1, -2}, {1, 3, -2}, {2, 3, 1},   {3, -2, 1},  {-2, 3, -1}, {3, 2, -1}};
+// Alg. 2 OutOrder and DodecantCoords.
+const int8_t kOutOrder[12][3] = {{-2, -1, 3}, {-1, 2, 3}, {2, 1, 3},  {1, -2, 3}, {2, 1, 3},  {1, -2, 3},
+                                 {-1, 2, 3},  {-2, -1, 3}, {2, 1, 3}, {-1, 2, 3}, {1, -2, 3}, {-2, -1, 3}};
+const int8_t kCoords[12][2] = {{1, 1}, {1, 2}, {2, 2}, {2, 1}, {0, 2}, {0, 1},
+                               {3, 2}, {3, 1}, {2, 0}, {1, 0}, {2, 3}, {1, 3}};
+
+const int8_t (*table_rows(int table, int transform))[3] {
+    if (table == DRT3D_TABLE_HEMISPHERE) return transform == 0 ? kDrtHemisphere : kDjtHemisphere;
+    if (table == DRT3D_TABLE_PRINTED) return kDrtPrinted;
+    if (table == DRT3D_TABLE_SHARED) return kShared;
+    return nullptr;
+}
+
+// reading A: oriented axis j = original axis |p_j| (1=x, 2=y, 3=z),
+// reversed when p_j < 0.  Original strides: x N^2, y N, z 1.
+Orient make_orient(const int8_t row[3], int N, int dod) {
+    Orient o{};
+    long long stride[3] = {(long long)N * N, (long long)N, 1};
+    long long s[3];
+    o.off0 = 0;
+    o.fast = 0;
+    for (int j = 0; j < 3; ++j) {
+        const int a = (row[j] < 0 ? -row[j] : row[j]) - 1;
+        if (row[j] > 0) s[j] = stride[a];
+        else { s[j] = -stride[a]; o.off0 += (long long)(N - 1) * stride[a]; }
+        if (a == 2) o.fast = j;
+    }
+    o.sx = s[0];
+    o.sy = s[1];
+    o.sz = s[2];
+    o.dod = dod;
+    return o;
+}
+
+// ------------------------------------------------------------ planning ------
+int stor_bytes(int s) { return s == ST_U8 ? 1 : s == ST_U16 ? 2 : 4; }
+int round_up(int a, int b) { return (a + b - 1) / b * b; }
+
+struct Plan {
+    int transform;          // 0 DRT, 1 DJT
+    int N, n, batch, ndod, inst;
+    int npass;
+    int ks[4];              // radix bits of each pass
+    int cs[5];              // bits done before pass p (cs[npass] = n)
+    int stor[5];            // storage type of stage cs[p] (stor[0] = input dtype)
+    int base[5], width[5], pitch[5];
+    long long plane[5];     // DJT: elements per plane
+    long long inst_elems[5];// elements per instance of stage buffers
+    int chunk;              // instances per chunk
+    size_t buf_bytes;       // one intermediate buffer (chunk instances)
+    int nbuf;
+    size_t ws_bytes;
+    int nlaunch;
+};
+
+const size_t kChunkBudget = 64ull << 20;   // keep a chunk's intermediates L2-resident (126 MB L2)
+
+int ilog2_exact(int N) {
+    if (N < 2 || N > 1024) return -1;
+    int n = 0;
+    while ((1 << n) < N) ++n;
+    return (1 << n) == N ? n : -1;
+}
+
+drt3d_opts default_opts() {
+    drt3d_opts o{};
+    o.batch = 1;
+    o.in_dtype = DRT3D_U8;
+    o.out_dtype = DRT3D_I32;
+    o.layout = DRT3D_LAYOUT_STACKED;
+    o.table = DRT3D_TABLE_HEMISPHERE;
+    return o;
+}
+
+int popcount12(uint32_t m) {
+    int c = 0;
+    for (int k = 0; k < 12; ++k) c += (m >> k) & 1;
+    return c;
+}
+
+drt3d_status make_plan(int transform, int N, uint32_t mask, const drt3d_opts &o, Plan &P) {
+    std::memset(&P, 0, sizeof(P));
+    const int n = ilog2_exact(N);
+    if (n < 0) return DRT3D_ERR_INVALID_ARG;
+    if (mask == 0 || mask >= (1u << 12)) return DRT3D_ERR_INVALID_ARG;
+    if (o.batch < 1) return DRT3D_ERR_INVALID_ARG;
+    const bool dt_ok = (o.in_dtype == DRT3D_U8 && o.out_dtype == DRT3D_I32) ||
+                       (o.in_dtype == DRT3D_I32 && o.out_dtype == DRT3D_I32) ||
+                       (o.in_dtype == DRT3D_F32 && o.out_dtype == DRT3D_F32);
+    if (!dt_ok) return DRT3D_ERR_INVALID_ARG;
+    if (o.table < 0 || o.table > 2) return DRT3D_ERR_INVALID_ARG;
+    if (o.layout != DRT3D_LAYOUT_STACKED && o.layout != DRT3D_LAYOUT_MOSAIC) return DRT3D_ERR_INVALID_ARG;
+    if (o.layout == DRT3D_LAYOUT_MOSAIC && (transform != 0 || mask != 0xFFFu)) return DRT3D_ERR_INVALID_ARG;
+
+    P.transform = transform;
+    P.N = N;
+    P.n = n;
+    P.batch = o.batch;
+    P.ndod = popcount12(mask);
+    P.inst = P.batch * P.ndod;
+    // pass radices: <= 4 stages per pass, the first pass takes the larger half
+    if (n <= 4) { P.npass = 1; P.ks[0] = n; }
+    else if (n <= 8) { P.npass = 2; P.ks[0] = (n + 1) / 2; P.ks[1] = n / 2; }
+    else { P.npass = 3; P.ks[0] = 4; P.ks[1] = (n - 3) / 2; P.ks[2] = n - 4 - P.ks[1]; }
+    P.cs[0] = 0;
+    for (int p = 0; p < P.npass; ++p) P.cs[p + 1] = P.cs[p] + P.ks[p];
+
+    P.stor[0] = o.in_dtype == DRT3D_U8 ? ST_U8 : o.in_dtype == DRT3D_I32 ? ST_U32 : ST_F32;
+    for (int p = 1; p <= P.npass; ++p) {
+        const int c = P.cs[p];
+        if (o.in_dtype == DRT3D_F32) P.stor[p] = ST_F32;
+        else if (o.in_dtype == DRT3D_I32) P.stor[p] = ST_U32;
+        else {
+            // u8 voxels: a stage-c partial sum adds 4^c (planes) or 2^c (lines)
+            // voxels <= 255, which fits 16 bits while 255 * count < 2^16.
+            const long long cnt = transform == 0 ? (1LL << (2 * c)) : (1LL << c);
+            P.stor[p] = (p < P.npass && 255LL * cnt < 65536LL) ? ST_U16 : ST_U32;
+        }
+        if (transform == 0) {
+            if (p == P.npass) { P.base[p] = 0; P.width[p] = 3 * N; P.pitch[p] = 3 * N; }
+            else {
+                P.base[p] = 2 * N - 2 * ((1 << c) - 1);
+                P.width[p] = N + 2 * ((1 << c) - 1);
+                P.pitch[p] = round_up(P.width[p], 32);
+            }
+            P.inst_elems[p] = (long long)N * N * P.pitch[p];
+        } else {
+            if (p == P.npass) { P.base[p] = 0; P.width[p] = 2 * N; P.pitch[p] = 2 * N; }
+            else {
+                P.base[p] = N - ((1 << c) - 1);
+                P.width[p] = N + (1 << c) - 1;
+                P.pitch[p] = round_up(P.width[p], 8);
+            }
+            P.plane[p] = (long long)P.width[p] * P.pitch[p];
+            P.inst_elems[p] = (long long)N * (1LL << c) * P.plane[p];
+        }
+    }
+    P.base[0] = transform == 0 ? 2 * N : N;
+    P.width[0] = N;
+    size_t per_inst = 0;
+    for (int p = 1; p < P.npass; ++p) {
+        const size_t b = (size_t)P.inst_elems[p] * stor_bytes(P.stor[p]);
+        if (b > per_inst) per_inst = b;
+    }
+    if (P.npass == 1) { P.chunk = P.inst; P.nbuf = 0; P.buf_bytes = 0; }
+    else {
+        long long ch = (long long)(kChunkBudget / (per_inst ? per_inst : 1));
+        if (ch < 1) ch = 1;
+        if (ch > P.inst) ch = P.inst;
+        if (ch > 65535) ch = 65535;
+        P.chunk = (int)ch;
+        P.nbuf = P.npass >= 3 ? 2 : 1;
+        P.buf_bytes = ((per_inst * (size_t)P.chunk + 255) / 256) * 256;
+    }
+    P.ws_bytes = P.buf_bytes * P.nbuf;
+    const int nchunks = (P.inst + P.chunk - 1) / P.chunk;
+    P.nlaunch = nchunks * P.npass + ((o.layout == DRT3D_LAYOUT_MOSAIC) ? 4 : 0);
+    return DRT3D_OK;
+}
+
+// ------------------------------------------------------------ launching -----
+struct Launcher {
+    cudaStream_t stream;
+    const drt3d_opts *o;
+    int count = 0;
+    template <class F>
+    drt3d_status run(int kind, F &&launch) {
+        cudaEvent_t *ev = o && o->events ? reinterpret_cast<cudaEvent_t *>(o->events) : nullptr;
+        const bool rec = ev && count < o->max_events;
+        if (rec) cudaEventRecord(ev[2 * count], stream);
+        launch();
+        if (rec) cudaEventRecord(ev[2 * count + 1], stream);
+        if (o && o->launch_kind && count < o->max_events) o->launch_kind[count] = kind;
+        ++count;
+        return cudaGetLastError() == cudaSuccess ? DRT3D_OK : DRT3D_ERR_CUDA;
+    }
+};
+
+drt3d_status dispatch_drt(int in_dtype, int K, int sin, int sout, bool first, bool fin, const DrtPass &prm, int ninst,
+                          cudaStream_t st) {
+    if (in_dtype == DRT3D_U8) return dispatch_drt_u8(K, sin, sout, first, fin, prm, ninst, st);
+    if (in_dtype == DRT3D_I32) return dispatch_drt_i32(K, sin, sout, first, fin, prm, ninst, st);
+    return dispatch_drt_f32(K, sin, sout, first, fin, prm, ninst, st);
+}
+drt3d_status dispatch_djt(int in_dtype, int K, int sin, int sout, bool first, bool fin, const DjtPass &prm, int ninst,
+                          cudaStream_t st) {
+    if (in_dtype == DRT3D_U8) return dispatch_djt_u8(K, sin, sout, first, fin, prm, ninst, st);
+    if (in_dtype == DRT3D_I32) return dispatch_djt_i32(K, sin, sout, first, fin, prm, ninst, st);
+    return dispatch_djt_f32(K, sin, sout, first, fin, prm, ninst, st);
+}
+
+size_t out_elems(int transform, const Plan &P, const drt3d_opts &o) {
+    const size_t N = (size_t)P.N;
+    if (transform == 0) {
+        if (o.layout == DRT3D_LAYOUT_MOSAIC) return (size_t)P.batch * 16 * N * N * (3 * N - 2);
+        return (size_t)P.inst * N * N * 3 * N;
+    }
+    return (size_t)P.inst * N * N * 4 * N * N;
+}
+
+int in_bytes(int dt) { return dt == DRT3D_U8 ? 1 : 4; }
+
+drt3d_status check_ptrs(const void *cube, void *out, void *ws, size_t ws_bytes, const Plan &P, const drt3d_opts &o,
+                        int transform) {
+    if (!cube || !out) return DRT3D_ERR_INVALID_ARG;
+    if ((reinterpret_cast<uintptr_t>(out) & 15) != 0) return DRT3D_ERR_INVALID_ARG;
+    const size_t cb = (size_t)P.batch * P.N * P.N * P.N * in_bytes(o.in_dtype);
+    const size_t ob = out_elems(transform, P, o) * 4;
+    const uintptr_t c0 = reinterpret_cast<uintptr_t>(cube), o0 = reinterpret_cast<uintptr_t>(out);
+    if (c0 < o0 + ob && o0 < c0 + cb) return DRT3D_ERR_INVALID_ARG;   // overlap
+    if (P.ws_bytes > 0) {
+        if (!ws || ws_bytes < P.ws_bytes) return DRT3D_ERR_WORKSPACE;
+        if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return DRT3D_ERR_INVALID_ARG;
+    }
+    return DRT3D_OK;
+}
+
+drt3d_status run_drt(const void *cube, uint32_t mask, void *out, const drt3d_opts &o, const Plan &P, void *ws,
+                     cudaStream_t st) {
+    const int8_t(*rows)[3] = table_rows(o.table, 0);
+    DrtPass base{};
+    base.N = P.N;
+    base.n = P.n;
+    base.ndod = P.ndod;
+    base.layout = o.layout;
+    int j = 0;
+    for (int k = 0; k < 12; ++k)
+        if ((mask >> k) & 1) {
+            base.ori[j] = make_orient(rows[k], P.N, k);
+            base.out_order[j][0] = kOutOrder[k][0];
+            base.out_order[j][1] = kOutOrder[k][1];
+            base.coords[j][0] = kCoords[k][0];
+            base.coords[j][1] = kCoords[k][1];
+            ++j;
+        }
+    Launcher L{st, &o};
+    char *buf[2] = {reinterpret_cast<char *>(ws), reinterpret_cast<char *>(ws) + P.buf_bytes};
+    const long long final_inst = (o.layout == DRT3D_LAYOUT_MOSAIC) ? 0 : (long long)P.N * P.N * 3 * P.N;
+    for (int i0 = 0; i0 < P.inst; i0 += P.chunk) {
+        const int ninst = (P.inst - i0) < P.chunk ? (P.inst - i0) : P.chunk;
+        for (int p = 0; p < P.npass; ++p) {
+            const bool first = p == 0, fin = p == P.npass - 1;
+            DrtPass prm = base;
+            prm.c = P.cs[p];
+            prm.m = P.n - P.cs[p + 1];
+            prm.inst0 = i0;
+            prm.in = first ? cube : buf[(p - 1) & 1];
+            prm.in_inst_stride = first ? 0 : P.inst_elems[p];
+            prm.in_pitch = P.pitch[p];
+            prm.in_base = P.base[p];
+            prm.in_width = P.width[p];
+            prm.out = fin ? out : buf[p & 1];
+            prm.out_inst_stride = fin ? final_inst : P.inst_elems[p + 1];
+            prm.out_pitch = P.pitch[p + 1];
+            prm.out_base = P.base[p + 1];
+            prm.out_width = P.width[p + 1];
+            drt3d_status s = DRT3D_OK;
+            drt3d_status ls = L.run(first ? 0 : (fin ? 2 : 1), [&] {
+                s = dispatch_drt(o.in_dtype, P.ks[p], P.stor[p], P.stor[p + 1], first, fin, prm, ninst, st);
+            });
+            if (s != DRT3D_OK) return s;
+            if (ls != DRT3D_OK) return ls;
+        }
+    }
+    if (o.layout == DRT3D_LAYOUT_MOSAIC) {
+        // the 4 blocks of the 4x4 grid no dodecant occupies
+        for (int bi = 0; bi < 4; ++bi)
+            for (int bj = 0; bj < 4; ++bj) {
+                bool used = false;
+                for (int k = 0; k < 12; ++k) used |= (kCoords[k][0] == bi && kCoords[k][1] == bj);
+                if (used) continue;
+                drt3d_status ls = L.run(3, [&] {
+                    mosaic_fill_kernel<<<P.batch * P.N * P.N, 128, 0, st>>>(out, P.N, P.batch, 4, bi, bj);
+                });
+                if (ls != DRT3D_OK) return ls;
+            }
+    }
+    if (o.launches) *o.launches = L.count;
+    return DRT3D_OK;
+}
+
+drt3d_status run_djt(const void *cube, uint32_t mask, void *out, const drt3d_opts &o, const Plan &P, void *ws,
+                     cudaStream_t st) {
+    const int8_t(*rows)[3] = table_rows(o.table, 1);
+    DjtPass base{};
+    base.N = P.N;
+    base.n = P.n;
+    base.ndod = P.ndod;
+    int j = 0;
+    for (int k = 0; k < 12; ++k)
+        if ((mask >> k) & 1) base.ori[j++] = make_orient(rows[k], P.N, k);
+    Launcher L{st, &o};
+    char *buf[2] = {reinterpret_cast<char *>(ws), reinterpret_cast<char *>(ws) + P.buf_bytes};
+    for (int i0 = 0; i0 < P.inst; i0 += P.chunk) {
+        const int ninst = (P.inst - i0) < P.chunk ? (P.inst - i0) : P.chunk;
+        for (int p = 0; p < P.npass; ++p) {
+            const bool first = p == 0, fin = p == P.npass - 1;
+            DjtPass prm = base;
+            prm.c = P.cs[p];
+            prm.m = P.n - P.cs[p + 1];
+            prm.inst0 = i0;
+            prm.in = first ? cube : buf[(p - 1) & 1];
+            prm.in_inst_stride = first ? 0 : P.inst_elems[p];
+            prm.in_plane = first ? 0 : P.plane[p];
+            prm.in_pitch = P.pitch[p];
+            prm.in_base = P.base[p];
+            prm.in_width = P.width[p];
+            prm.out = fin ? out : buf[p & 1];
+            prm.out_inst_stride = P.inst_elems[p + 1];
+            prm.out_plane = P.plane[p + 1];
+            prm.out_pitch = P.pitch[p + 1];
+            prm.out_base = P.base[p + 1];
+            prm.out_width = P.width[p + 1];
+            drt3d_status s = DRT3D_OK;
+            drt3d_status ls = L.run(first ? 0 : (fin ? 2 : 1), [&] {
+                s = dispatch_djt(o.in_dtype, P.ks[p], P.stor[p], P.stor[p + 1], first, fin, prm, ninst, st);
+            });
+            if (s != DRT3D_OK) return s;
+            if (ls != DRT3D_OK) return ls;
+        }
+    }
+    if (o.launches) *o.launches = L.count;
+    return DRT3D_OK;
+}
+
+const drt3d_opts &opts_or_default(const drt3d_opts *o, drt3d_opts &tmp) {
+    if (o) return *o;
+    tmp = default_opts();
+    return tmp;
+}
+
+}  // namespace
+
+// ============================================================== C ABI =======
+extern "C" {
+
+const char *drt3d_status_string(drt3d_status s) {
+    switch (s) {
+        case DRT3D_OK: return "DRT3D_OK";
+        case DRT3D_ERR_INVALID_ARG: return "DRT3D_ERR_INVALID_ARG";
+        case DRT3D_ERR_UNSUPPORTED: return "DRT3D_ERR_UNSUPPORTED";
+        case DRT3D_ERR_WORKSPACE: return "DRT3D_ERR_WORKSPACE";
+        case DRT3D_ERR_CUDA: return "DRT3D_ERR_CUDA";
+    }
+    return "DRT3D_ERR_UNKNOWN";
+}
+
+drt3d_status drt3d_orientation_table(int table, int transform, int8_t rows[36]) {
+    if (!rows || transform < 0 || transform > 1) return DRT3D_ERR_INVALID_ARG;
+    const int8_t(*t)[3] = table_rows(table, transform);
+    if (!t) return DRT3D_ERR_INVALID_ARG;
+    for (int k = 0; k < 12; ++k)
+        for (int j = 0; j < 3; ++j) rows[3 * k + j] = t[k][j];
+    return DRT3D_OK;
+}
+
+size_t drt3d_planes_out_elems(int N, uint32_t mask, const drt3d_opts *opts) {
+    drt3d_opts tmp;
+    const drt3d_opts &o = opts_or_default(opts, tmp);
+    Plan P;
+    if (make_plan(0, N, mask, o, P) != DRT3D_OK) return 0;
+    return out_elems(0, P, o);
+}
+
+drt3d_status drt3d_planes_workspace_size(int N, uint32_t mask, const drt3d_opts *opts, size_t *bytes) {
+    if (!bytes) return DRT3D_ERR_INVALID_ARG;
+    drt3d_opts tmp;
+    const drt3d_opts &o = opts_or_default(opts, tmp);
+    Plan P;
+    drt3d_status s = make_plan(0, N, mask, o, P);
+    if (s != DRT3D_OK) return s;
+    *bytes = P.ws_bytes;
+    return DRT3D_OK;
+}
+
+drt3d_status drt3d_planes(const void *cube, int N, uint32_t mask, void *out, const drt3d_opts *opts,
+                          void *workspace, size_t workspace_bytes, void *stream) {
+    drt3d_opts tmp;
+    const drt3d_opts &o = opts_or_default(opts, tmp);
+    Plan P;
+    drt3d_status s = make_plan(0, N, mask, o, P);
+    if (s != DRT3D_OK) return s;
+    s = check_ptrs(cube, out, workspace, workspace_bytes, P, o, 0);
+    if (s != DRT3D_OK) return s;
+    return run_drt(cube, mask, out, o, P, workspace, reinterpret_cast<cudaStream_t>(stream));
+}
+
+size_t djt3d_lines_out_elems(int N, uint32_t mask, const drt3d_opts *opts) {
+    drt3d_opts tmp;
+    const drt3d_opts &o = opts_or_default(opts, tmp);
+    Plan P;
+    if (make_plan(1, N, mask, o, P) != DRT3D_OK) return 0;
+    return out_elems(1, P, o);
+}
+
+drt3d_status djt3d_lines_workspace_size(int N, uint32_t mask, const drt3d_opts *opts, size_t *bytes) {
+    if (!bytes) return DRT3D_ERR_INVALID_ARG;
+    drt3d_opts tmp;
+    const drt3d_opts &o = opts_or_default(opts, tmp);
+    Plan P;
+    drt3d_status s = make_plan(1, N, mask, o, P);
+    if (s != DRT3D_OK) return s;
+    *bytes = P.ws_bytes;
+    return DRT3D_OK;
+}
+
+drt3d_status djt3d_lines(const void *cube, int N, uint32_t mask, void *out, const drt3d_opts *opts, void *workspace,
+                         size_t workspace_bytes, void *stream) {
+    drt3d_opts tmp;
+    const drt3d_opts &o = opts_or_default(opts, tmp);
+    Plan P;
+    drt3d_status s = make_plan(1, N, mask, o, P);
+    if (s != DRT3D_OK) return s;
+    s = check_ptrs(cube, out, workspace, workspace_bytes, P, o, 1);
+    if (s != DRT3D_OK) return s;
+    return run_djt(cube, mask, out, o, P, workspace, reinterpret_cast<cudaStream_t>(stream));
+}
+
+static drt3d_status host_variant(int transform, const void *host_cube, int N, uint32_t mask, void *host_out,
+                                 const drt3d_opts *opts, void *dev_cube, void *dev_out, void *ws, size_t ws_bytes,
+                                 void *stream) {
+    drt3d_opts tmp;
+    const drt3d_opts &o = opts_or_default(opts, tmp);
+    Plan P;
+    drt3d_status s = make_plan(transform, N, mask, o, P);
+    if (s != DRT3D_OK) return s;
+    if (!host_cube || !host_out) return DRT3D_ERR_INVALID_ARG;
+    s = check_ptrs(dev_cube, dev_out, ws, ws_bytes, P, o, transform);
+    if (s != DRT3D_OK) return s;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const size_t cb = (size_t)P.batch * N * N * N * in_bytes(o.in_dtype);
+    const size_t ob = out_elems(transform, P, o) * 4;
+    if (cudaMemcpyAsync(dev_cube, host_cube, cb, cudaMemcpyHostToDevice, st) != cudaSuccess) return DRT3D_ERR_CUDA;
+    s = transform == 0 ? run_drt(dev_cube, mask, dev_out, o, P, ws, st) : run_djt(dev_cube, mask, dev_out, o, P, ws, st);
+    if (s != DRT3D_OK) return s;
+    if (cudaMemcpyAsync(host_out, dev_out, ob, cudaMemcpyDeviceToHost, st) != cudaSuccess) return DRT3D_ERR_CUDA;
+    return DRT3D_OK;
+}
+
+drt3d_status drt3d_planes_host(const void *host_cube, int N, uint32_t mask, void *host_out, const drt3d_opts *opts,
+                               void *dev_cube, void *dev_out, void *ws, size_t ws_bytes, void *stream) {
+    return host_variant(0, host_cube, N, mask, host_out, opts, dev_cube, dev_out, ws, ws_bytes, stream);
+}
+
+drt3d_status djt3d_lines_host(const void *host_cube, int N, uint32_t mask, void *host_out, const drt3d_opts *opts,
+                              void *dev_cube, void *dev_out, void *ws, size_t ws_bytes, void *stream) {
+    return host_variant(1, host_cube, N, mask, host_out, opts, dev_cube, dev_out, ws, ws_bytes, stream);
+}
+
+}  // extern "C"

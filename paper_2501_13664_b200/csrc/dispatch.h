@@ -1,0 +1,18 @@
+// dispatch.h -- per-dtype kernel dispatch entry points (defined in k_*.cu).
+#pragma once
+#include "drt3d.h"
+#include "common.cuh"
+#include "djt_kernels.cuh"
+#include "drt_kernels.cuh"
+
+namespace d3 {
+#define D3_DECL(NAME, PASS) \
+    drt3d_status NAME(int K, int sin, int sout, bool first, bool fin, const PASS &prm, int ninst, cudaStream_t st);
+D3_DECL(dispatch_drt_u8, DrtPass)
+D3_DECL(dispatch_drt_i32, DrtPass)
+D3_DECL(dispatch_drt_f32, DrtPass)
+D3_DECL(dispatch_djt_u8, DjtPass)
+D3_DECL(dispatch_djt_i32, DjtPass)
+D3_DECL(dispatch_djt_f32, DjtPass)
+#undef D3_DECL
+}  // namespace d3

@@ -1,0 +1,201 @@
+// djt_kernels.cuh -- 3D DJT of lines: one "radix-2^K pass" kernel.
+//
+// Alg. 3 (eq:map3DJ PAPER.md:425-437) regrouped into passes
+// of K stages.  From the stage-c partial transform (eq:3DJfm)
+// the stage-(c+K) value is a direct sum over 2^K consecutive rows along the
+// driving axis:
+//
+//   f^{c+K}(V | s1' | s2' | D1 | D2) = sum_{w < 2^K} f^c(V 2^K + w | s1 | s2 |
+//               D1 + s1 w + l^K_{r1}(w) | D2 + s2 w + l^K_{r2}(w)),   s' = s 2^K + r.
+//
+// Storage of a stage-c buffer (per instance):
+//   rows ((s1 2^c + s2) 2^(n-c) + v), each a plane [D1'][D2'],
+//   Di' = Di - base_c, base_c = N - (2^c - 1), valid width N + 2^c - 1.
+// Stage 0 is the oriented cube (x' = v, D1 = y' + N, D2 = z' + N), the final
+// stage is out[s1][s2][D1][D2] with Di in [0, 2N) (Alg. 3 + separateS1S2).
+#pragma once
+#include "common.cuh"
+
+namespace d3 {
+
+struct DjtPass {
+    const void *in;
+    void *out;
+    int N, n, c, m;
+    long long in_inst_stride, in_plane;    // elements between instances / rows (planes)
+    int in_pitch, in_base, in_width;
+    long long out_inst_stride, out_plane;
+    int out_pitch, out_base, out_width;
+    int nt2;                               // tiles along D2
+    int inst0, ndod;
+    Orient ori[kMaxDod];
+};
+
+template <int K, int R, int T1, int T2>
+struct DjtGeom {
+    static constexpr int S = 1 << K;
+    static constexpr int H = S - 1;
+    static constexpr int WR = T1 + H;                     // staged rows per plane
+    static constexpr int WC = T2 + H;                     // staged columns
+    static constexpr int NR = T2 / R;
+    static constexpr int NEED = ((T2 + H + 3) / 4) * 4;   // furthest column touched
+    static constexpr int PJ0 = ((NEED > WC ? NEED : WC) + 3) / 4 * 4;
+    static constexpr int PJ = ((PJ0 / 4) % 2 == 1) ? PJ0 : PJ0 + 4;   // pitch/4 odd: no bank conflicts across rows
+    static constexpr int TASKS = S * T1 * NR;
+    static constexpr int THREADS = 256;
+    static constexpr int SMEM = S * WR * PJ * 4;
+    static_assert(T2 % R == 0 && R % 4 == 0, "tile shape");
+};
+
+template <int K, int R, int T1, int T2, class In, class Acc, class Out, bool FIRST, bool FINAL>
+__global__ void __launch_bounds__(256)
+djt_pass_kernel(const DjtPass p) {
+    using G = DjtGeom<K, R, T1, T2>;
+    constexpr int S = G::S, WR = G::WR, WC = G::WC, PJ = G::PJ, NR = G::NR;
+    extern __shared__ uint4 smem_u4[];
+    uint32_t *sm = reinterpret_cast<uint32_t *>(smem_u4);
+
+    const int tid = threadIdx.x;
+    const int t1 = blockIdx.x / p.nt2, t2 = blockIdx.x - t1 * p.nt2;
+    const int g = blockIdx.y, li = blockIdx.z, inst = p.inst0 + li;
+    const int m = p.m, c = p.c, N = p.N, cK = c + K;
+    const int V = g & ((1 << m) - 1);
+    const int sig = g >> m;
+    const int sg2 = sig & ((1 << c) - 1), sg1 = sig >> c;
+    const int d10 = t1 * T1, d20 = t2 * T2;                 // stored output coords of the tile
+    const int D1abs = p.out_base + d10, D2abs = p.out_base + d20;
+
+    Out *outp = reinterpret_cast<Out *>(p.out);
+    const long long out_inst = FINAL ? (long long)inst * p.out_inst_stride : (long long)li * p.out_inst_stride;
+    auto out_plane_ptr = [&](int r1, int r2) -> Out * {
+        const int s1 = (sg1 << K) + r1, s2 = (sg2 << K) + r2;
+        const long long row = ((((long long)s1 << cK) + s2) << m) + V;
+        return outp + out_inst + row * p.out_plane;
+    };
+
+    // ---- zero tiles: outputs need Di >= N - si (line support)
+    {
+        const int s1max = (sg1 << K) + S - 1, s2max = (sg2 << K) + S - 1;
+        if (D1abs + T1 <= N - s1max || D2abs + T2 <= N - s2max) {
+            for (int i = tid; i < S * S * T1 * T2; i += blockDim.x) {
+                const int e2 = i % T2, rest = i / T2, e1 = rest % T1, pl = rest / T1;
+                if (d10 + e1 < p.out_width && d20 + e2 < p.out_width)
+                    out_plane_ptr(pl / S, pl % S)[(long long)(d10 + e1) * p.out_pitch + d20 + e2] = to_out<Out, Acc>(Acc(0));
+            }
+            return;
+        }
+    }
+
+    // ---- stage the 2^K input planes' windows
+    if constexpr (FIRST) {
+        const Orient o = p.ori[inst % p.ndod];
+        const In *cube = reinterpret_cast<const In *>(p.in) + (long long)(inst / p.ndod) * N * N * N;
+        const int y0 = D1abs - N, z0 = D2abs - N;     // stage 0: D1 = y' + N, D2 = z' + N
+        const int xb = V << K;
+        for (int i = tid; i < S * WR * WC; i += blockDim.x) {
+            int w, i1, i2;
+            if (o.fast == 2) { i2 = i % WC; const int rw = i / WC; i1 = rw % WR; w = rw / WR; }
+            else if (o.fast == 0) { w = i % S; const int rw = i / S; i2 = rw % WC; i1 = rw / WC; }
+            else { i1 = i % WR; const int rw = i / WR; i2 = rw % WC; w = rw / WC; }
+            const int y = y0 + i1, z = z0 + i2;
+            uint32_t bits = 0;
+            if ((unsigned)y < (unsigned)N && (unsigned)z < (unsigned)N)
+                bits = Elem<In>::load_bits(cube + o.off0 + (xb + w) * o.sx + y * o.sy + z * o.sz);
+            sm[(w * WR + i1) * PJ + i2] = bits;
+        }
+    } else {
+        const In *inb = reinterpret_cast<const In *>(p.in) + (long long)li * p.in_inst_stride;
+        const int nc = p.n - c;
+        const long long rbase = ((((long long)sg1 << c) + sg2) << nc) + ((long long)V << K);
+        for (int i = tid; i < S * WR * WC; i += blockDim.x) {
+            const int i2 = i % WC, rest = i / WC, i1 = rest % WR, w = rest / WR;
+            const int a1 = D1abs + sg1 * w - p.in_base + i1;
+            const int a2 = D2abs + sg2 * w - p.in_base + i2;
+            uint32_t bits = 0;
+            if ((unsigned)a1 < (unsigned)p.in_width && (unsigned)a2 < (unsigned)p.in_width)
+                bits = Elem<In>::load_bits(inb + (rbase + w) * p.in_plane + (long long)a1 * p.in_pitch + a2);
+            sm[(w * WR + i1) * PJ + i2] = bits;
+        }
+    }
+    __syncthreads();
+
+    // ---- direct sum: thread task (r1, d1, run) accumulates all S values of r2
+    constexpr int NB = (R + S + 2) / 4;
+    for (int task = tid; task < G::TASKS; task += blockDim.x) {
+        const int d1 = task % T1, rest = task / T1, rr = rest % NR, r1 = rest / NR;
+        const int c0 = rr * (R / 4);
+        Acc acc[S][R];
+#pragma unroll
+        for (int r = 0; r < S; ++r)
+#pragma unroll
+            for (int j = 0; j < R; ++j) acc[r][j] = Acc(0);
+        static_for<0, S>([&](auto w_) {
+            constexpr int w = decltype(w_)::value;
+            constexpr int NC = (R + w + 3) / 4;
+            // l^K_{r1}(w) at run time (r1 is a per-thread value; only a row offset)
+            int l1 = 0;
+            {
+                int s = r1, u = w;
+#pragma unroll
+                for (int k = K; k >= 1; --k) {
+                    l1 += ((u >> (k - 1)) & 1) * ((s + 1) >> 1);
+                    s >>= 1;
+                    u &= (1 << (k - 1)) - 1;
+                }
+            }
+            const uint32_t *row = sm + (w * WR + d1 + l1) * PJ + c0 * 4;
+            uint32_t buf[NB * 4];
+#pragma unroll
+            for (int i = 0; i < NC; ++i) {
+                const uint4 v = *reinterpret_cast<const uint4 *>(row + 4 * i);
+                buf[4 * i + 0] = v.x;
+                buf[4 * i + 1] = v.y;
+                buf[4 * i + 2] = v.z;
+                buf[4 * i + 3] = v.w;
+            }
+            static_for<0, S>([&](auto r_) {
+                constexpr int r = decltype(r_)::value;
+                constexpr int off = lk(K, r, w);
+#pragma unroll
+                for (int j = 0; j < R; ++j) acc[r][j] = acc[r][j] + Lane<Acc>::get(buf[j + off]);
+            });
+        });
+        // store S output planes (r1, r2), row d1, columns run rr
+        const int e1 = d10 + d1, e2 = d20 + rr * R;
+        if (e1 < p.out_width) {
+            const bool vec_ok = (e2 + R <= p.out_width) && ((p.out_pitch * (int)sizeof(Out)) % 16 == 0) &&
+                                ((e2 * (int)sizeof(Out)) % 16 == 0) && ((p.out_plane * (long long)sizeof(Out)) % 16 == 0);
+#pragma unroll
+            for (int r2 = 0; r2 < S; ++r2) {
+                Out *dst = out_plane_ptr(r1, r2) + (long long)e1 * p.out_pitch + e2;
+                if (vec_ok) {
+                    if constexpr (sizeof(Out) == 2) {
+#pragma unroll
+                        for (int q = 0; q < R / 8; ++q) {
+                            uint32_t wv[4];
+#pragma unroll
+                            for (int h = 0; h < 4; ++h)
+                                wv[h] = (uint32_t)to_out<Out, Acc>(acc[r2][8 * q + 2 * h]) |
+                                        ((uint32_t)to_out<Out, Acc>(acc[r2][8 * q + 2 * h + 1]) << 16);
+                            *reinterpret_cast<uint4 *>(dst + 8 * q) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                        }
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < R / 4; ++q) {
+                            const uint32_t a0 = Lane<Acc>::bits(acc[r2][4 * q + 0]), a1 = Lane<Acc>::bits(acc[r2][4 * q + 1]);
+                            const uint32_t a2 = Lane<Acc>::bits(acc[r2][4 * q + 2]), a3 = Lane<Acc>::bits(acc[r2][4 * q + 3]);
+                            if (FINAL) st_cs_v4(dst + 4 * q, a0, a1, a2, a3);
+                            else *reinterpret_cast<uint4 *>(dst + 4 * q) = make_uint4(a0, a1, a2, a3);
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < R; ++j)
+                        if (e2 + j < p.out_width) dst[j] = to_out<Out, Acc>(acc[r2][j]);
+                }
+            }
+        }
+    }
+}
+
+}  // namespace d3

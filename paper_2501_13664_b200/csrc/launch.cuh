@@ -1,0 +1,85 @@
+// launch.cuh -- kernel launch templates (tile shapes per radix) shared by
+// the per-dtype translation units k_*.cu.
+#pragma once
+#include "dispatch.h"
+
+namespace d3 {
+
+template <class KernelT>
+bool set_smem(KernelT k, int bytes) {
+    if (bytes <= 48 * 1024) return true;
+    return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess;
+}
+
+// ---- DRT kernel selection
+template <int K> struct DrtTile;
+template <> struct DrtTile<1> { static constexpr int R = 8, T = 128; };
+template <> struct DrtTile<2> { static constexpr int R = 8, T = 128; };
+template <> struct DrtTile<3> { static constexpr int R = 8, T = 64; };
+template <> struct DrtTile<4> { static constexpr int R = 8, T = 64; };
+
+template <int K, class In, class Acc, class Out, bool FIRST, bool FINAL>
+drt3d_status launch_drt_k(const DrtPass &prm, int ninst, cudaStream_t st) {
+    constexpr int R = DrtTile<K>::R, T = DrtTile<K>::T;
+    using G = DrtGeom<K, R, T>;
+    auto kern = drt_pass_kernel<K, R, T, In, Acc, Out, FIRST, FINAL>;
+    static bool attr_ok = set_smem(kern, G::SMEM);
+    if (!attr_ok) return DRT3D_ERR_CUDA;
+    const int ntiles = (prm.out_width + T - 1) / T;
+    const long long groups = 1LL << (2 * (prm.c + prm.m));
+    dim3 grid(ntiles, (unsigned)groups, ninst);
+    kern<<<grid, G::THREADS, G::SMEM, st>>>(prm);
+    return DRT3D_OK;
+}
+
+template <class In, class Acc, class Out, bool FIRST, bool FINAL>
+drt3d_status launch_drt(int K, const DrtPass &prm, int ninst, cudaStream_t st) {
+    switch (K) {
+        case 1: return launch_drt_k<1, In, Acc, Out, FIRST, FINAL>(prm, ninst, st);
+        case 2: return launch_drt_k<2, In, Acc, Out, FIRST, FINAL>(prm, ninst, st);
+        case 3: return launch_drt_k<3, In, Acc, Out, FIRST, FINAL>(prm, ninst, st);
+        case 4: return launch_drt_k<4, In, Acc, Out, FIRST, FINAL>(prm, ninst, st);
+    }
+    return DRT3D_ERR_UNSUPPORTED;
+}
+
+// ---- DJT kernel selection
+template <int K> struct DjtTile;
+template <> struct DjtTile<1> { static constexpr int R = 8, T1 = 8, T2 = 64; };
+template <> struct DjtTile<2> { static constexpr int R = 8, T1 = 8, T2 = 64; };
+template <> struct DjtTile<3> { static constexpr int R = 8, T1 = 8, T2 = 64; };
+template <> struct DjtTile<4> { static constexpr int R = 8, T1 = 4, T2 = 64; };
+
+template <int K, class In, class Acc, class Out, bool FIRST, bool FINAL>
+drt3d_status launch_djt_k(DjtPass prm, int ninst, cudaStream_t st) {
+    constexpr int R = DjtTile<K>::R, T1 = DjtTile<K>::T1, T2 = DjtTile<K>::T2;
+    using G = DjtGeom<K, R, T1, T2>;
+    auto kern = djt_pass_kernel<K, R, T1, T2, In, Acc, Out, FIRST, FINAL>;
+    static bool attr_ok = set_smem(kern, G::SMEM);
+    if (!attr_ok) return DRT3D_ERR_CUDA;
+    const int nt1 = (prm.out_width + T1 - 1) / T1, nt2 = (prm.out_width + T2 - 1) / T2;
+    prm.nt2 = nt2;
+    const long long groups = (1LL << (2 * prm.c)) << prm.m;
+    dim3 grid(nt1 * nt2, (unsigned)groups, ninst);
+    kern<<<grid, G::THREADS, G::SMEM, st>>>(prm);
+    return DRT3D_OK;
+}
+
+template <class In, class Acc, class Out, bool FIRST, bool FINAL>
+drt3d_status launch_djt(int K, const DjtPass &prm, int ninst, cudaStream_t st) {
+    switch (K) {
+        case 1: return launch_djt_k<1, In, Acc, Out, FIRST, FINAL>(prm, ninst, st);
+        case 2: return launch_djt_k<2, In, Acc, Out, FIRST, FINAL>(prm, ninst, st);
+        case 3: return launch_djt_k<3, In, Acc, Out, FIRST, FINAL>(prm, ninst, st);
+        case 4: return launch_djt_k<4, In, Acc, Out, FIRST, FINAL>(prm, ninst, st);
+    }
+    return DRT3D_ERR_UNSUPPORTED;
+}
+
+
+}  // namespace d3
+
+#define D3_DRT_CASE(SI, SO, F, L, IT, AT, OT) \
+    if (sin == SI && sout == SO && first == F && fin == L) return launch_drt<IT, AT, OT, F, L>(K, prm, ninst, st);
+#define D3_DJT_CASE(SI, SO, F, L, IT, AT, OT) \
+    if (sin == SI && sout == SO && first == F && fin == L) return launch_djt<IT, AT, OT, F, L>(K, prm, ninst, st);

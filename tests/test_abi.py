@@ -1,0 +1,91 @@
+"""CPU-side checks of the C-ABI library: it loads, exports every symbol the
+header declares, and its host-only entry points (tables, sizes, validation)
+behave as documented.  No kernel is launched here."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2501_13664_b200 as d3
+from oracle import tables
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    from paper_2501_13664_b200 import build
+    build.build()
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "drt3d.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return set(re.findall(r"\b((?:drt3d|djt3d)_[a-z_]+)\s*\(", src))
+
+
+def test_exports_every_declared_symbol():
+    names = _declared()
+    assert names == set(d3.C_FUNCTIONS)
+    L = d3.lib()
+    for n in names:
+        assert hasattr(L, n), n
+
+
+def test_orientation_tables_match_oracle_copy():
+    # the library and the oracle each hold their own copy (R6-R8)
+    assert d3.orientation_table(d3.DRT3D_TABLE_HEMISPHERE, 0) == tables.DRT_HEMISPHERE
+    assert d3.orientation_table(d3.DRT3D_TABLE_HEMISPHERE, 1) == tables.DJT_HEMISPHERE
+    assert d3.orientation_table(d3.DRT3D_TABLE_PRINTED, 0) == tables.DRT_PRINTED
+    assert d3.orientation_table(d3.DRT3D_TABLE_PRINTED, 1) == tables.DRT_PRINTED
+    assert d3.orientation_table(d3.DRT3D_TABLE_SHARED, 0) == tables.SHARED
+
+
+def test_out_elems():
+    o = d3.make_opts()
+    assert d3.drt3d_planes_out_elems(256, 0xFFF, o) == 12 * 256 * 256 * 768
+    assert d3.drt3d_planes_out_elems(16, 0x1, o) == 16 * 16 * 48
+    o5 = d3.make_opts(batch=256, in_dtype=d3.DRT3D_F32, out_dtype=d3.DRT3D_F32)
+    assert d3.drt3d_planes_out_elems(32, 0xFFF, o5) == 256 * 12 * 32 * 32 * 96
+    om = d3.make_opts(layout=d3.DRT3D_LAYOUT_MOSAIC)
+    assert d3.drt3d_planes_out_elems(8, 0xFFF, om) == 32 * 32 * 22
+    assert d3.djt3d_lines_out_elems(64, 0x1, o) == 64 * 64 * 128 * 128
+    assert d3.drt3d_planes_out_elems(12, 0x1, o) == 0        # invalid N
+
+
+def test_workspace_sizes():
+    o = d3.make_opts()
+    assert d3.drt3d_planes_workspace_size(16, 0x1, o) == 0  # single pass, no intermediate
+    ws = d3.drt3d_planes_workspace_size(256, 0xFFF, o)
+    # one N=256 dodecant's stage-4 buffer: N^2 rows x pitch 288 x u16
+    assert ws >= 256 * 256 * 288 * 2
+    assert ws < 200 << 20
+    assert d3.djt3d_lines_workspace_size(64, 0x1, o) > 0
+
+
+@pytest.mark.parametrize("N,mask,kw,err", [
+    (12, 0x1, {}, d3.DRT3D_ERR_INVALID_ARG),
+    (1, 0x1, {}, d3.DRT3D_ERR_INVALID_ARG),
+    (2048, 0x1, {}, d3.DRT3D_ERR_INVALID_ARG),
+    (16, 0x0, {}, d3.DRT3D_ERR_INVALID_ARG),
+    (16, 0x1000, {}, d3.DRT3D_ERR_INVALID_ARG),
+    (16, 0x1, dict(in_dtype=d3.DRT3D_U8, out_dtype=d3.DRT3D_F32), d3.DRT3D_ERR_INVALID_ARG),
+    (16, 0x1, dict(batch=0), d3.DRT3D_ERR_INVALID_ARG),
+    (16, 0x1, dict(layout=d3.DRT3D_LAYOUT_MOSAIC), d3.DRT3D_ERR_INVALID_ARG),   # mosaic needs 0xFFF
+    (16, 0x1, dict(table=7), d3.DRT3D_ERR_INVALID_ARG),
+])
+def test_validation_rejects_before_launch(N, mask, kw, err):
+    o = d3.make_opts(**kw)
+    # bogus device pointers: validation must fail before anything touches them
+    assert d3.drt3d_planes(16, N, mask, 1 << 40, o, None, 0, None) == err
+
+
+def test_null_and_workspace_errors():
+    o = d3.make_opts()
+    assert d3.drt3d_planes(None, 16, 1, 1 << 40, o, None, 0, None) == d3.DRT3D_ERR_INVALID_ARG
+    assert d3.drt3d_planes(16, 16, 1, None, o, None, 0, None) == d3.DRT3D_ERR_INVALID_ARG
+    assert d3.drt3d_planes(16, 256, 1, 1 << 40, o, None, 0, None) == d3.DRT3D_ERR_WORKSPACE
+    assert d3.djt3d_lines(16, 64, 1, 1 << 40, o, None, 0, None) == d3.DRT3D_ERR_WORKSPACE
+    assert d3.djt3d_lines(16, 64, 1, (1 << 40) + 4, o, None, 0, None) == d3.DRT3D_ERR_INVALID_ARG  # misaligned out
+    assert d3.status_string(d3.DRT3D_ERR_CUDA) == "DRT3D_ERR_CUDA"

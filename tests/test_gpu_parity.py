@@ -1,0 +1,241 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Integer configs must match bit for bit; the float config within the
+tolerance DESIGN.md derives (|gpu - ref64| <= 1e-5 * sum|terms|, C-amb-14).
+Inputs are the seeded synthetic cubes of synth/ (BASELINE.json configs 1-5).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from oracle import tables
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2501_13664_b200 as d3  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    d3.lib()
+    yield
+
+
+def _gpu(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _4d(a):
+    return a[None] if a.ndim == 3 else a
+
+
+def _planes(cube, mask, **kw):
+    out = d3.planes(_gpu(_4d(cube)), mask, **kw)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+def _lines(cube, mask, **kw):
+    out = d3.lines(_gpu(_4d(cube)), mask, **kw)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+# ------------------------------------------------------------ 3D DRT
+
+def test_cfg1_n16_i32_dodecant0():
+    cube = synth.config_input(1)                       # [1][16][16][16] int32
+    got = _planes(cube, 0x001)
+    ref = oracle.drt_planes(cube, 0x001)
+    assert got.dtype == np.int32 and got.shape == (1, 1, 16, 16, 48)
+    assert np.array_equal(got.astype(np.int64), ref)
+
+
+@pytest.mark.parametrize("N", [2, 4, 8, 16, 32, 64, 128])
+@pytest.mark.parametrize("dtype", [np.uint8, np.int32])
+def test_drt_random_all_dodecants(N, dtype):
+    if N == 128 and dtype == np.int32:
+        pytest.skip("covered by the uint8 case; keeps the oracle time bounded")
+    lo, hi = (0, 255) if dtype == np.uint8 else (-1000, 1000)
+    cube = synth.uniform_cube(N, 100 + N, dtype, lo, hi, batch=2 if N <= 32 else 1)
+    got = _planes(cube, 0xFFF)
+    ref = oracle.drt_planes(cube, 0xFFF)
+    assert np.array_equal(got.astype(np.int64), ref)
+
+
+@pytest.mark.parametrize("table", [d3.DRT3D_TABLE_PRINTED, d3.DRT3D_TABLE_SHARED])
+@pytest.mark.parametrize("N", [8, 64])
+def test_drt_other_tables(N, table):
+    cube = synth.uniform_cube(N, 200 + N, np.uint8)
+    got = _planes(cube, 0xFFF, table=table)
+    ref = oracle.drt_planes(cube, 0xFFF, table)
+    assert np.array_equal(got.astype(np.int64), ref)
+
+
+@pytest.mark.parametrize("mask", [0x001, 0x020, 0x210, 0x801, 0xAAA])
+def test_drt_masks(mask):
+    cube = synth.uniform_cube(32, 300 + mask, np.uint8)
+    got = _planes(cube, mask)
+    ref = oracle.drt_planes(cube, mask)
+    assert np.array_equal(got.astype(np.int64), ref)
+
+
+def test_cfg2_n64_sheets_full():
+    cube = synth.config_input(2)
+    got = _planes(cube, 0xFFF)
+    ref = oracle.drt_planes(cube, 0xFFF)
+    assert np.array_equal(got.astype(np.int64), ref)
+
+
+def test_cfg3_n256_full_size():
+    """BASELINE config 3 at full size, same launch as bench.py: two dodecants
+    against the full oracle recursion, every dodecant on sampled outputs
+    (eq:3DfDRT by direct summation) and on invariants (mass, support)."""
+    cube = synth.config_input(3)
+    N = 256
+    gpu = d3.planes(_gpu(cube), 0xFFF)[0]             # cube is [1][N][N][N] -> [12][N][N][3N] int32 on device
+    torch.cuda.synchronize()
+    f = cube[0]
+    # mass: each (s1, s2) column sums to the cube total
+    tot = int(f.astype(np.int64).sum())
+    sums = gpu.to(torch.int64).sum(dim=3)
+    assert bool((sums == tot).all())
+    # support: zero below D = 2N - s1 - s2
+    s = torch.arange(N, device="cuda")
+    lim = 2 * N - s[:, None] - s[None, :]
+    D = torch.arange(3 * N, device="cuda")
+    below = D[None, None, :] < lim[:, :, None]
+    assert int(gpu.masked_select(below.unsqueeze(0).expand_as(gpu)).abs().sum()) == 0
+    host = gpu.cpu().numpy()
+    rows = tables.DRT_HEMISPHERE
+    for k in (0, 5):
+        ref = oracle.drt_alg1(oracle.orient(f, rows[k]))
+        assert np.array_equal(host[k].astype(np.int64), ref)
+    rng = np.random.default_rng(3)
+    for k in range(12):
+        g = oracle.orient(f, rows[k])
+        for _ in range(40):
+            s1, s2 = int(rng.integers(0, N)), int(rng.integers(0, N))
+            Dd = int(rng.integers(2 * N - s1 - s2, 3 * N))
+            assert host[k, s1, s2, Dd] == oracle.drt_point(g, s1, s2, Dd)
+
+
+def test_cfg5_batched_f32():
+    """Config 5: 256 cubes N=32 f32, 12 dodecants.  Tolerance (T1):
+    |gpu - ref64| <= 1e-5 * sum|terms| per element, sum|terms| = the fp64
+    transform of |f|; empty planes must be exactly 0."""
+    cube = synth.config_input(5)                       # [256][32][32][32] f32
+    got = _planes(cube, 0xFFF)                         # [256][12][32][32][96]
+    assert got.dtype == np.float32 and np.isfinite(got).all()
+    for b in (0, 1, 77, 255):
+        ref = oracle.drt_planes(cube[b].astype(np.float64), 0xFFF)
+        refabs = oracle.drt_planes(np.abs(cube[b]).astype(np.float64), 0xFFF)
+        err = np.abs(got[b].astype(np.float64) - ref)
+        assert np.all(err <= 1e-5 * refabs)
+        assert np.all(got[b][refabs == 0] == 0)
+    # the rest: sampled outputs by direct summation
+    rng = np.random.default_rng(5)
+    rows = tables.DRT_HEMISPHERE
+    for _ in range(300):
+        b, k = int(rng.integers(0, 256)), int(rng.integers(0, 12))
+        s1, s2, D = (int(t) for t in rng.integers(0, [32, 32, 96]))
+        g = oracle.orient(cube[b].astype(np.float64), rows[k])
+        ref, scale = oracle.drt_point(g, s1, s2, D), oracle.drt_point(g, s1, s2, D, absolute=True)
+        assert abs(float(got[b, k, s1, s2, D]) - ref) <= 1e-5 * scale
+
+
+def test_drt_float_small_all_tables():
+    cube = synth.normal_cube(16, 9, batch=3)
+    got = _planes(cube, 0xFFF)
+    for b in range(3):
+        ref = oracle.drt_planes(cube[b].astype(np.float64), 0xFFF)
+        refabs = oracle.drt_planes(np.abs(cube[b]).astype(np.float64), 0xFFF)
+        assert np.all(np.abs(got[b] - ref) <= 1e-5 * refabs)
+
+
+def test_drt_mosaic_layout():
+    for N in (4, 32):
+        cube = synth.uniform_cube(N, 400 + N, np.uint8)
+        got = _planes(cube, 0xFFF, layout=d3.DRT3D_LAYOUT_MOSAIC)
+        assert got.shape == (1, 4 * N, 4 * N, 3 * N - 2)
+        ref = oracle.mosaic(oracle.drt_planes(cube, 0xFFF))
+        assert np.array_equal(got[0].astype(np.int64), ref)
+
+
+def test_drt_edge_cases():
+    # zero cube -> zeros; delta at origin -> 1 at D = 2N for all slopes
+    N = 64
+    z = np.zeros((N, N, N), np.uint8)
+    assert not _planes(z, 0xFFF).any()
+    z[0, 0, 0] = 1
+    got = _planes(z, 0x001)[0, 0]
+    exp = np.zeros_like(got)
+    exp[:, :, 2 * N] = 1
+    assert np.array_equal(got, exp)
+    # maximum voxels: 255 everywhere at N=256 reaches 255 N^2 = 16.7M (fits int32)
+    full = np.full((1, 256, 256, 256), 255, np.uint8)
+    g = d3.planes(_gpu(full), 0x001)
+    torch.cuda.synchronize()
+    assert int(g[0, 0, 0, 0, 2 * 256]) == 255 * 256 * 256
+    assert int(g.max()) == 255 * 256 * 256
+
+
+def test_drt_deterministic():
+    cube = synth.uniform_cube(64, 7, np.uint8)
+    a = _planes(cube, 0xFFF)
+    b = _planes(cube, 0xFFF)
+    assert np.array_equal(a, b)
+
+
+def test_drt_int32_wraps_mod_2_32():
+    # int32 output = exact sum mod 2^32 (include/drt3d.h)
+    N = 8
+    cube = np.full((N, N, N), 2 ** 30, np.int32)
+    got = _planes(cube, 0x001)
+    ref = oracle.drt_planes(cube.astype(np.int64), 0x001)
+    assert np.array_equal(got.astype(np.int64), ((ref + 2 ** 31) % 2 ** 32) - 2 ** 31)
+
+
+# ------------------------------------------------------------ 3D DJT
+
+def test_cfg4_djt_n64_full():
+    cube = synth.config_input(4)
+    got = _lines(cube, 0x001)
+    ref = oracle.djt_lines(cube, 0x001)
+    assert got.shape == (1, 1, 64, 64, 128, 128)
+    assert np.array_equal(got.astype(np.int64), ref)
+
+
+@pytest.mark.parametrize("N", [2, 4, 8, 16, 32])
+@pytest.mark.parametrize("dtype", [np.uint8, np.int32, np.float32])
+def test_djt_random_all_dodecants(N, dtype):
+    if dtype == np.float32:
+        cube = synth.normal_cube(N, 500 + N, batch=2)
+    else:
+        cube = synth.uniform_cube(N, 500 + N, dtype, 0, 255, batch=2)
+    got = _lines(cube, 0xFFF)
+    if dtype == np.float32:
+        for b in range(2):
+            ref = oracle.djt_lines(cube[b].astype(np.float64), 0xFFF)
+            refabs = oracle.djt_lines(np.abs(cube[b]).astype(np.float64), 0xFFF)
+            assert np.all(np.abs(got[b] - ref) <= 1e-5 * refabs)
+    else:
+        ref = oracle.djt_lines(cube, 0xFFF)
+        assert np.array_equal(got.astype(np.int64), ref)
+
+
+def test_djt_n128_sampled():
+    N = 128
+    cube = synth.uniform_cube(N, 600, np.uint8)
+    gpu = d3.lines(_gpu(cube[None]), 0x001)[0, 0]
+    torch.cuda.synchronize()
+    assert bool((gpu.to(torch.int64).sum(dim=(2, 3)) == int(cube.astype(np.int64).sum())).all())
+    host = gpu.cpu().numpy()
+    rng = np.random.default_rng(6)
+    for _ in range(300):
+        s1, s2, D1, D2 = (int(t) for t in rng.integers(0, [N, N, 2 * N, 2 * N]))
+        assert host[s1, s2, D1, D2] == oracle.djt_point(cube, s1, s2, D1, D2)
