@@ -164,9 +164,13 @@ drt3d_status make_plan(int transform, int N, uint32_t mask, const drt3d_opts &o,
         if (transform == 0) {
             if (p == P.npass) { P.base[p] = 0; P.width[p] = 3 * N; P.pitch[p] = 3 * N; }
             else {
-                P.base[p] = 2 * N - 2 * ((1 << c) - 1);
-                P.width[p] = N + 2 * ((1 << c) - 1);
-                P.pitch[p] = round_up(P.width[p], 32);
+                // stage-c support starts at D = 2N - 2(2^c - 1) (eq:3Dfm); the stored
+                // origin is rounded down to 16 so that the next pass' tiles start 16-aligned, and
+                // rows are computed (zero-padded) up to their pitch so any 16-byte chunk inside a
+                // row is valid data.
+                P.base[p] = (2 * N - 2 * ((1 << c) - 1)) / 16 * 16;
+                P.pitch[p] = round_up(3 * N - P.base[p], 16);
+                P.width[p] = P.pitch[p];
             }
             P.inst_elems[p] = (long long)N * N * P.pitch[p];
         } else {
@@ -249,6 +253,7 @@ drt3d_status check_ptrs(const void *cube, void *out, void *ws, size_t ws_bytes, 
                         int transform) {
     if (!cube || !out) return DRT3D_ERR_INVALID_ARG;
     if ((reinterpret_cast<uintptr_t>(out) & 15) != 0) return DRT3D_ERR_INVALID_ARG;
+    if ((reinterpret_cast<uintptr_t>(cube) & 15) != 0) return DRT3D_ERR_INVALID_ARG;
     const size_t cb = (size_t)P.batch * P.N * P.N * P.N * in_bytes(o.in_dtype);
     const size_t ob = out_elems(transform, P, o) * 4;
     const uintptr_t c0 = reinterpret_cast<uintptr_t>(cube), o0 = reinterpret_cast<uintptr_t>(out);
@@ -268,6 +273,7 @@ drt3d_status run_drt(const void *cube, uint32_t mask, void *out, const drt3d_opt
     base.n = P.n;
     base.ndod = P.ndod;
     base.layout = o.layout;
+    base.vec_ok = (P.N >= 16) ? 1 : 0;
     int j = 0;
     for (int k = 0; k < 12; ++k)
         if ((mask >> k) & 1) {
@@ -331,6 +337,7 @@ drt3d_status run_djt(const void *cube, uint32_t mask, void *out, const drt3d_opt
     base.N = P.N;
     base.n = P.n;
     base.ndod = P.ndod;
+    base.vec_ok = (P.N >= 16) ? 1 : 0;
     int j = 0;
     for (int k = 0; k < 12; ++k)
         if ((mask >> k) & 1) base.ori[j++] = make_orient(rows[k], P.N, k);

@@ -64,6 +64,69 @@ __device__ __forceinline__ void st_cs_v4(void *p, uint32_t a, uint32_t b, uint32
     asm volatile("st.global.cs.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 
+// ---------------------------------------------------------------------------
+// Staging of row segments into shared memory with batched 16-byte loads.
+// Row r supplies elements j = st + dir*e, e in [0, W), of a contiguous source
+// row `ptr` whose valid indices are [0, width) (others read as 0).  Each thread
+// first issues up to ITEMS independent LDG.128 (chunk-aligned), then scatters
+// the elements through dst(r, e, bits): load latency is overlapped instead of
+// serialised element by element.
+template <class In>
+struct RowSrc {
+    const In *ptr;
+    int st, dir, width;
+};
+
+template <class In>
+__device__ __forceinline__ uint32_t chunk_elem(const uint4 &v, int q) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    if constexpr (sizeof(In) == 1) return (w[q >> 2] >> (8 * (q & 3))) & 0xFFu;
+    else if constexpr (sizeof(In) == 2) return (w[q >> 1] >> (16 * (q & 1))) & 0xFFFFu;
+    else return w[q];
+}
+
+__device__ __forceinline__ int floor_div(int a, int b) { return (a >= 0) ? a / b : -((-a + b - 1) / b); }
+
+template <class In, int ITEMS, class RowFn, class DstFn>
+__device__ __forceinline__ void stage_rows(int nrows, int W, RowFn &&rowfn, DstFn &&dst) {
+    constexpr int EPC = 16 / (int)sizeof(In);
+    const int nch = (W + EPC - 1) / EPC + 1;
+    const int items = nrows * nch;
+    const int nthr = blockDim.x;
+    for (int base = threadIdx.x; base < items; base += nthr * ITEMS) {
+        uint4 v[ITEMS];
+        int cbs[ITEMS], rs[ITEMS];
+        RowSrc<In> src[ITEMS];
+#pragma unroll
+        for (int u = 0; u < ITEMS; ++u) {
+            const int it = base + u * nthr;
+            v[u] = make_uint4(0u, 0u, 0u, 0u);
+            rs[u] = -1;
+            if (it < items) {
+                const int r = it / nch, ch = it - r * nch;
+                const RowSrc<In> ri = rowfn(r);
+                const int jlo = ri.dir > 0 ? ri.st : ri.st - W + 1;
+                const int cb = floor_div(jlo, EPC) * EPC + ch * EPC;
+                rs[u] = r;
+                cbs[u] = cb;
+                src[u] = ri;
+                if (cb >= 0 && cb < ri.width) v[u] = __ldg(reinterpret_cast<const uint4 *>(ri.ptr + cb));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < ITEMS; ++u) {
+            if (rs[u] < 0) continue;
+            const RowSrc<In> ri = src[u];
+#pragma unroll
+            for (int q = 0; q < EPC; ++q) {
+                const int j = cbs[u] + q;
+                const int e = ri.dir > 0 ? j - ri.st : ri.st - j;
+                if (e >= 0 && e < W) dst(rs[u], e, (j >= 0 && j < ri.width) ? chunk_elem<In>(v[u], q) : 0u);
+            }
+        }
+    }
+}
+
 // Oriented-cube addressing (Alg. 2 permute + flip as an index remap,
 // PAPER.md:342-348, reading A): element (x', y', z') of dodecant k lives at
 // off0 + x'*sx + y'*sy + z'*sz in the original [x][y][z] cube.  fast = the

@@ -28,6 +28,7 @@ struct DjtPass {
     int out_pitch, out_base, out_width;
     int nt2;                               // tiles along D2
     int inst0, ndod;
+    int vec_ok;                            // first pass: 16-byte chunked cube loads are aligned
     Orient ori[kMaxDod];
 };
 
@@ -87,35 +88,59 @@ djt_pass_kernel(const DjtPass p) {
     }
 
     // ---- stage the 2^K input planes' windows
+    auto put = [&](int w, int i1, int i2, uint32_t bits) { sm[(w * WR + i1) * PJ + i2] = bits; };
     if constexpr (FIRST) {
         const Orient o = p.ori[inst % p.ndod];
         const In *cube = reinterpret_cast<const In *>(p.in) + (long long)(inst / p.ndod) * N * N * N;
         const int y0 = D1abs - N, z0 = D2abs - N;     // stage 0: D1 = y' + N, D2 = z' + N
         const int xb = V << K;
-        for (int i = tid; i < S * WR * WC; i += blockDim.x) {
-            int w, i1, i2;
-            if (o.fast == 2) { i2 = i % WC; const int rw = i / WC; i1 = rw % WR; w = rw / WR; }
-            else if (o.fast == 0) { w = i % S; const int rw = i / S; i2 = rw % WC; i1 = rw / WC; }
-            else { i1 = i % WR; const int rw = i / WR; i2 = rw % WC; w = rw / WC; }
-            const int y = y0 + i1, z = z0 + i2;
-            uint32_t bits = 0;
-            if ((unsigned)y < (unsigned)N && (unsigned)z < (unsigned)N)
-                bits = Elem<In>::load_bits(cube + o.off0 + (xb + w) * o.sx + y * o.sy + z * o.sz);
-            sm[(w * WR + i1) * PJ + i2] = bits;
+        auto run = [&](long long b, long long stride, int start, bool valid) {
+            RowSrc<In> r;
+            if (stride > 0) { r.ptr = cube + b; r.st = start; r.dir = 1; }
+            else { r.ptr = cube + b - (N - 1); r.st = N - 1 - start; r.dir = -1; }
+            r.width = valid ? N : 0;
+            return r;
+        };
+        if (!p.vec_ok) {
+            for (int i = tid; i < S * WR * WC; i += blockDim.x) {
+                const int i2 = i % WC, rest = i / WC, i1 = rest % WR, w = rest / WR;
+                const int y = y0 + i1, z = z0 + i2;
+                uint32_t bits = 0;
+                if ((unsigned)y < (unsigned)N && (unsigned)z < (unsigned)N)
+                    bits = Elem<In>::load_bits(cube + o.off0 + (xb + w) * o.sx + y * o.sy + z * o.sz);
+                put(w, i1, i2, bits);
+            }
+        } else if (o.fast == 2) {           // z' (D2) contiguous
+            stage_rows<In, 8>(S * WR, WC, [&](int r) {
+                const int i1 = r % WR, w = r / WR, y = y0 + i1;
+                return run(o.off0 + (long long)(xb + w) * o.sx + (long long)y * o.sy, o.sz, z0, (unsigned)y < (unsigned)N);
+            }, [&](int r, int i2, uint32_t bits) { put(r / WR, r % WR, i2, bits); });
+        } else if (o.fast == 1) {           // y' (D1) contiguous
+            stage_rows<In, 8>(S * WC, WR, [&](int r) {
+                const int i2 = r % WC, w = r / WC, z = z0 + i2;
+                return run(o.off0 + (long long)(xb + w) * o.sx + (long long)z * o.sz, o.sy, y0, (unsigned)z < (unsigned)N);
+            }, [&](int r, int i1, uint32_t bits) { put(r / WC, i1, r % WC, bits); });
+        } else {                            // x' (driving axis) contiguous
+            stage_rows<In, 8>(WR * WC, S, [&](int r) {
+                const int i2 = r % WC, i1 = r / WC, y = y0 + i1, z = z0 + i2;
+                return run(o.off0 + (long long)y * o.sy + (long long)z * o.sz, o.sx, xb,
+                           (unsigned)y < (unsigned)N && (unsigned)z < (unsigned)N);
+            }, [&](int r, int w, uint32_t bits) { put(w, r / WC, r % WC, bits); });
         }
     } else {
         const In *inb = reinterpret_cast<const In *>(p.in) + (long long)li * p.in_inst_stride;
         const int nc = p.n - c;
         const long long rbase = ((((long long)sg1 << c) + sg2) << nc) + ((long long)V << K);
-        for (int i = tid; i < S * WR * WC; i += blockDim.x) {
-            const int i2 = i % WC, rest = i / WC, i1 = rest % WR, w = rest / WR;
+        stage_rows<In, 8>(S * WR, WC, [&](int r) {
+            const int i1 = r % WR, w = r / WR;
             const int a1 = D1abs + sg1 * w - p.in_base + i1;
-            const int a2 = D2abs + sg2 * w - p.in_base + i2;
-            uint32_t bits = 0;
-            if ((unsigned)a1 < (unsigned)p.in_width && (unsigned)a2 < (unsigned)p.in_width)
-                bits = Elem<In>::load_bits(inb + (rbase + w) * p.in_plane + (long long)a1 * p.in_pitch + a2);
-            sm[(w * WR + i1) * PJ + i2] = bits;
-        }
+            RowSrc<In> rr;
+            rr.ptr = inb + (rbase + w) * p.in_plane + (long long)a1 * p.in_pitch;
+            rr.st = D2abs + sg2 * w - p.in_base;
+            rr.dir = 1;
+            rr.width = ((unsigned)a1 < (unsigned)p.in_width) ? p.in_width : 0;
+            return rr;
+        }, [&](int r, int i2, uint32_t bits) { put(r / WR, r % WR, i2, bits); });
     }
     __syncthreads();
 

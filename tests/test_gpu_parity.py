@@ -34,15 +34,18 @@ def _4d(a):
 
 
 def _planes(cube, mask, **kw):
+    """[B][N][N][N] -> [B][K]...; a 3D cube -> [K]... (the oracle's convention)."""
     out = d3.planes(_gpu(_4d(cube)), mask, **kw)
     torch.cuda.synchronize()
-    return out.cpu().numpy()
+    res = out.cpu().numpy()
+    return res[0] if cube.ndim == 3 else res
 
 
 def _lines(cube, mask, **kw):
     out = d3.lines(_gpu(_4d(cube)), mask, **kw)
     torch.cuda.synchronize()
-    return out.cpu().numpy()
+    res = out.cpu().numpy()
+    return res[0] if cube.ndim == 3 else res
 
 
 # ------------------------------------------------------------ 3D DRT
@@ -161,9 +164,9 @@ def test_drt_mosaic_layout():
     for N in (4, 32):
         cube = synth.uniform_cube(N, 400 + N, np.uint8)
         got = _planes(cube, 0xFFF, layout=d3.DRT3D_LAYOUT_MOSAIC)
-        assert got.shape == (1, 4 * N, 4 * N, 3 * N - 2)
+        assert got.shape == (4 * N, 4 * N, 3 * N - 2)
         ref = oracle.mosaic(oracle.drt_planes(cube, 0xFFF))
-        assert np.array_equal(got[0].astype(np.int64), ref)
+        assert np.array_equal(got.astype(np.int64), ref)
 
 
 def test_drt_edge_cases():
@@ -172,7 +175,7 @@ def test_drt_edge_cases():
     z = np.zeros((N, N, N), np.uint8)
     assert not _planes(z, 0xFFF).any()
     z[0, 0, 0] = 1
-    got = _planes(z, 0x001)[0, 0]
+    got = _planes(z, 0x001)[0]
     exp = np.zeros_like(got)
     exp[:, :, 2 * N] = 1
     assert np.array_equal(got, exp)
