@@ -191,6 +191,76 @@ drt_pass_kernel(const DrtPass p) {
                     bits = Elem<In>::load_bits(cube + o.off0 + (xb + w1) * o.sx + (yb + w2) * o.sy + z * o.sz);
                 put(slot, e, bits);
             }
+        } else if (sizeof(In) == 1 && o.fast == 2 && o.sz > 0 && (z0 & 15) == 0 && 16 * ((WIN + 15) / 16) <= PI) {
+            // u8 rows along z' (forward, 16-aligned): one LDG.128 = 16 voxels = 4 SMEM chunks
+            constexpr int NQ16 = (WIN + 15) / 16;
+            constexpr int ITEMS = 4;
+            for (int base = tid; base < S * S * NQ16; base += blockDim.x * ITEMS) {
+                uint4 v[ITEMS];
+                int sl[ITEMS], qq[ITEMS];
+#pragma unroll
+                for (int u = 0; u < ITEMS; ++u) {
+                    const int it = base + u * blockDim.x;
+                    v[u] = make_uint4(0u, 0u, 0u, 0u);
+                    sl[u] = -1;
+                    if (it < S * S * NQ16) {
+                        const int slot = it / NQ16, q = it - slot * NQ16;
+                        const int w1 = slot / S, w2 = slot - w1 * S, z = z0 + 16 * q;
+                        sl[u] = slot;
+                        qq[u] = q;
+                        if ((unsigned)z < (unsigned)N)
+                            v[u] = __ldg(reinterpret_cast<const uint4 *>(
+                                cube + o.off0 + (long long)(xb + w1) * o.sx + (long long)(yb + w2) * o.sy + z));
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < ITEMS; ++u) {
+                    if (sl[u] < 0) continue;
+                    const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+                    const int sw = swz<K>(sl[u]);
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        const uint4 o4 = make_uint4(__byte_perm(w[h], 0, 0x4440), __byte_perm(w[h], 0, 0x4441),
+                                                    __byte_perm(w[h], 0, 0x4442), __byte_perm(w[h], 0, 0x4443));
+                        *reinterpret_cast<uint4 *>(sm + sl[u] * PI + (((4 * qq[u] + h) ^ sw) << 2)) = o4;
+                    }
+                }
+            }
+        } else if (sizeof(In) == 1 && K == 4 && o.fast != 2) {
+            // u8, unit stride along x' (fast 0) or y' (fast 1): one LDG.128 = the 16 voxels of a
+            // run along that axis; 4 consecutive z' per item are transposed in registers so every
+            // SMEM write is a 16-byte chunk (4 consecutive e of one slot)
+            const bool fx = o.fast == 0;
+            const long long sf = fx ? o.sx : o.sy, so = fx ? o.sy : o.sx;
+            const int fb = fx ? xb : yb, ob = fx ? yb : xb;
+            constexpr int NG = (WIN + 3) / 4;
+            for (int it = tid; it < S * NG; it += blockDim.x) {
+                const int other = it % S, g = it / S;
+                uint4 v[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const int z = z0 + 4 * g + t;
+                    v[t] = make_uint4(0u, 0u, 0u, 0u);
+                    if ((unsigned)z < (unsigned)N) {
+                        const long long b = o.off0 + (long long)(ob + other) * so + (long long)z * o.sz +
+                                            (sf > 0 ? (long long)fb : -(long long)(fb + 15));
+                        v[t] = __ldg(reinterpret_cast<const uint4 *>(cube + b));
+                    }
+                }
+#pragma unroll
+                for (int wf = 0; wf < 16; ++wf) {
+                    const int byte = sf > 0 ? wf : 15 - wf;     // runtime-uniform direction
+                    uint32_t q4[4];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const uint32_t w[4] = {v[t].x, v[t].y, v[t].z, v[t].w};
+                        q4[t] = __byte_perm(w[byte >> 2], 0, 0x4440 | (byte & 3));
+                    }
+                    const int slot = fx ? wf * S + other : other * S + wf;
+                    *reinterpret_cast<uint4 *>(sm + slot * PI + ((g ^ swz<K>(slot)) << 2)) =
+                        make_uint4(q4[0], q4[1], q4[2], q4[3]);
+                }
+            }
         } else if (o.fast == 2) {
             // rows along z' are contiguous in the original cube (reversed when sz < 0)
             stage_rows<In, 8>(S * S, WIN, [&](int slot) {
@@ -339,6 +409,11 @@ struct DrtMidGeom {
     static constexpr int YT = S * NRY;
     static constexpr int THREADS = ((XT > YT ? XT : YT) + 31) / 32 * 32;
     static constexpr int SMEM = S * S * SP;
+    // two CTAs per SM: with W warps per CTA an SM sub-partition holds ceil(2W/4) warps of its
+    // 16K-register file, which caps the registers per thread
+    static constexpr int WARPS = THREADS / 32;
+    static constexpr int MAXREG0 = 16384 / (((2 * WARPS + 3) / 4) * 32) / 8 * 8;
+    static constexpr int MAXREG = MAXREG0 > 255 ? 255 : MAXREG0;
     static_assert(T % R == 0 && R % 4 == 0 && (R % EPC == 0 || EPC > R), "tile shape");
     static_assert((NRY - 1) * R + (R + H + 3) / 4 * 4 <= NRX * R, "y-step reads inside X");
 };
@@ -415,7 +490,7 @@ __device__ __forceinline__ void direct_sum2(LoadRow &&load_row, Acc (&acc)[1 << 
 }
 
 template <int K, int R, int T, class MidIn, class Acc, class Out, bool FINAL>
-__global__ void __launch_bounds__(DrtMidGeom<K, R, T, MidIn>::THREADS)
+__global__ void __maxnreg__((DrtMidGeom<K, R, T, MidIn>::MAXREG))
 drt_pass_mid_kernel(const DrtPass p) {
     using G = DrtMidGeom<K, R, T, MidIn>;
     constexpr int S = G::S, SP = G::SP, EPC = G::EPC, NQ = G::NQ;

@@ -40,6 +40,8 @@ bool make_row_tmap(CUtensorMap *m, const void *base, long long rows, int width, 
 
 template <class KernelT>
 bool set_smem(KernelT k, int bytes) {
+    // prefer the maximum shared-memory carveout so two CTAs of ~100 KB fit on one SM
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (bytes <= 48 * 1024) return true;
     return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess;
 }
