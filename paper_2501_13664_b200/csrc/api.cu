@@ -274,6 +274,7 @@ drt3d_status run_drt(const void *cube, uint32_t mask, void *out, const drt3d_opt
     base.ndod = P.ndod;
     base.layout = o.layout;
     base.vec_ok = (P.N >= 16) ? 1 : 0;
+    base.one = 1;
     int j = 0;
     for (int k = 0; k < 12; ++k)
         if ((mask >> k) & 1) {

@@ -13,17 +13,17 @@
 // The runtime part (s1 w1 + s2 w2) is applied when a row is staged into
 // shared memory; the compile-time part l^K_r(w) becomes register indexing in
 // two separable direct sums (x then y).  Each CTA owns one group and one D
-// tile of width T; all 4^K rows stay in shared memory.
+// tile of width T; all 4^K rows stay in shared memory as 32-bit lanes.
 //
 // Storage of a stage-c buffer (per instance = one (cube, dodecant) pair):
 //   rows  ((s1 2^c + s2) 2^(n-c) + v1) 2^(n-c) + v2,     (N^2 rows)
-//   D' = D - base_c, base_c = 2N - 2(2^c - 1), valid width W_c = N + 2(2^c - 1)
-// (the support of eq:3Dfm at stage c).  Stage 0 is the oriented cube
-// itself (base 2N, width N); the final stage is the stacked output
-// out[s1][s2][D], D in [0, 3N), zero outside the support.
+//   D' = D - base_c with base_c = floor16(2N - 2(2^c - 1)) (the support of
+//   eq:3Dfm at stage c starts at 2N - 2(2^c - 1)), rows computed and
+//   zero-padded up to their pitch.  Stage 0 is the oriented cube itself
+//   (base 2N, width N); the final stage is the stacked output out[s1][s2][D],
+//   D in [0, 3N), zero outside the support.
 #pragma once
 #include "common.cuh"
-#include "tma.cuh"
 
 namespace d3 {
 
@@ -39,71 +39,142 @@ struct DrtPass {
     int ndod;                       // dodecants per cube (instances per batch entry)
     int layout;                     // final pass: 0 stacked, 1 mosaic
     int vec_ok;                     // first pass: 16-byte chunked cube loads are aligned (N >= 16)
+    uint32_t one;                   // = 1; a runtime multiplier so some adds issue as IMAD (FMA pipe)
     Orient ori[kMaxDod];            // first pass: per-dodecant-slot orientation
     int8_t out_order[kMaxDod][2];   // mosaic: OutOrder[k][0..1]
     int8_t coords[kMaxDod][2];      // mosaic: DodecantCoords[k]
 };
 
-template <int K, int R, int T>
+template <int K, int R, int T, bool STAGE16 = false>
 struct DrtGeom {
     static constexpr int S = 1 << K;
-    static constexpr int H = S - 1;                      // max l^K_r(w) = w <= S-1
-    static constexpr int WIN = T + 2 * H;                // staged row width
-    static constexpr int NRX = (T + H + R - 1) / R;      // x-step runs per row
-    static constexpr int NRY = T / R;                    // y-step runs per row
-    static constexpr int NEED = (NRX - 1) * R + (R + H + 3) / 4 * 4;   // words touched by the last run
-    static constexpr int PI = ((NEED > WIN ? NEED : WIN) + 31) / 32 * 32;  // row pitch (words)
-    static constexpr int XT = S * NRX;                   // x-step tasks
-    static constexpr int YT = S * NRY;                   // y-step tasks
+    static constexpr int H = S - 1;                       // max l^K_r(w) = w <= S-1
+    static constexpr int WIN = T + 2 * H;                 // input elements a tile needs per row
+    static constexpr int NRX = (T + H + R - 1) / R;       // x-step runs per row (X needs T + H)
+    static constexpr int NRY = T / R;                     // y-step runs per row
+    static constexpr int EPS = STAGE16 ? 8 : 4;           // staged elements per 16-byte chunk
+    static constexpr int RD = (NRX - 1) * R + (R + H + EPS - 1) / EPS * EPS;   // staged elements the x-step touches
+    static constexpr int BW = ((WIN > RD ? WIN : RD) + 15) / 16 * 16; // staged elements per row
+    // slot layout (bytes): STAGE16 (u16 stage-c rows): [staged u16 | raw aligned source chunks],
+    // otherwise [staged 32-bit]; X (32-bit, NRX*R words, XOR-swizzled chunks) is written in place.
+    static constexpr int STAGED = BW * (STAGE16 ? 2 : 4);
+    static constexpr int RAWOFF = STAGED;
+    static constexpr int NRAW = STAGE16 ? BW / 8 + 1 : 0; // raw 16-byte chunks per slot
+    static constexpr int XB = NRX * R * 4;
+    static constexpr int SP0 = (STAGED + 16 * NRAW > XB ? STAGED + 16 * NRAW : XB);
+    static constexpr int SP = (SP0 + 15) / 16 * 16 + 16;  // slot pitch; +16 rotates banks per slot
+    static constexpr int XT = S * NRX;                    // x-step tasks
+    static constexpr int YT = S * NRY;                    // y-step tasks
     static constexpr int THREADS = ((XT > YT ? XT : YT) + 31) / 32 * 32;
-    static constexpr int SMEM = S * S * PI * 4;
-    static_assert(T % R == 0 && R % 4 == 0, "tile shape");
+    static constexpr int SMEM = S * S * SP;
+    // two CTAs per SM: with W warps per CTA one SM sub-partition holds ceil(2W/4) warps of its
+    // 16K-register file, which caps the registers per thread
+    static constexpr int WARPS = THREADS / 32;
+    static constexpr int MAXREG0 = 16384 / (((2 * WARPS + 3) / 4) * 32) / 8 * 8;
+    static constexpr int MAXREG = MAXREG0 > 255 ? 255 : MAXREG0;
+    static_assert(T % R == 0 && R % 8 == 0, "tile shape");
+    static_assert((NRY - 1) * R + (R + H + 3) / 4 * 4 <= NRX * R, "y-step reads inside X");
 };
 
-// XOR swizzle of 16-byte chunks inside each 128-byte group of a staged row:
-// makes the 8 lanes of an LDS.128 phase hit 8 distinct bank groups whether the
-// lanes vary the first or the second row coordinate.
-template <int K>
-__device__ __forceinline__ int swz(int slot) { return ((slot >> K) ^ slot) & 7; }
+// XOR swizzle of 16-byte chunks (flip bit 0 in every other 8-chunk group): lanes
+// that read runs R = 8 words apart (chunk stride 2) hit 8 distinct bank groups.
+__device__ __forceinline__ int xswz(int c) { return c ^ ((c >> 3) & 1); }
 
-// acc[r][j] += sum over the S rows a of row_a[j + l^K_r(a)], rows staged at
-// slot(a) = slot_base + a * slot_step, the thread's run starting at chunk c0.
-template <int K, int R, int PI, class Acc>
-__device__ __forceinline__ void drt_direct_sum(const uint32_t *__restrict__ sm, int slot_base, int slot_step,
-                                               int c0, Acc (&acc)[1 << K][R]) {
+// acc[r][j] += sum_a row_a[j + l^K_r(a)] over the S staged rows slot(a) =
+// slot0 + a * sstep; the thread's run starts at chunk c0.  Rows are taken two
+// at a time so the integer sums become 3-input adds.
+// Integer lanes: ~3/8 of the output rows take their two adds as IMAD x*one + acc
+// (FMA pipe, `one` a runtime 1) and the rest as one IADD3 (ALU pipe), so the
+// two integer-capable pipes share the work.
+template <class Acc>
+__device__ __forceinline__ Acc add2(Acc acc, uint32_t x, uint32_t y, uint32_t one, bool fma) {
+    if constexpr (std::is_same<Acc, uint32_t>::value) {
+        if (fma) return x * one + (y * one + acc);
+        return acc + x + y;
+    } else {
+        return acc + Lane<Acc>::get(x) + Lane<Acc>::get(y);
+    }
+}
+
+template <int K, int R, int SP, bool U16, class Acc>
+__device__ __forceinline__ void drt_accumulate(const unsigned char *__restrict__ sm, int slot0, int sstep, int c0,
+                                               uint32_t one, Acc (&acc)[1 << K][R]) {
     constexpr int S = 1 << K;
-    constexpr int NB = (R + S + 2) / 4;
-    static_for<0, S>([&](auto a_) {
-        constexpr int a = decltype(a_)::value;
-        constexpr int NC = (R + a + 3) / 4;              // chunks holding [run, run + R + a)
-        const int slot = slot_base + a * slot_step;
-        const int sw = swz<K>(slot);
-        const uint32_t *row = sm + slot * PI;
-        uint32_t buf[NB * 4];
+    // U16: unswizzled u16 rows, run start = chunk c0 (8 elements per chunk); else 32-bit
+    // rows with XOR-swizzled chunks, run start = chunk c0 (4 elements per chunk).
+    auto load = [&](int a, int ne, uint32_t *buf) {
+        const unsigned char *row = sm + (slot0 + a * sstep) * SP;
+        if constexpr (U16) {
 #pragma unroll
-        for (int i = 0; i < NC; ++i) {
-            const uint4 v = *reinterpret_cast<const uint4 *>(row + (((c0 + i) ^ sw) << 2));
-            buf[4 * i + 0] = v.x;
-            buf[4 * i + 1] = v.y;
-            buf[4 * i + 2] = v.z;
-            buf[4 * i + 3] = v.w;
+            for (int i = 0; i < (ne + 7) / 8; ++i) {
+                const uint4 v = *reinterpret_cast<const uint4 *>(row + 16 * (c0 + i));
+                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    if (8 * i + q < ne) buf[8 * i + q] = (q & 1) ? (w[q >> 1] >> 16) : (w[q >> 1] & 0xFFFFu);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < (ne + 3) / 4; ++i) {
+                const uint4 v = *reinterpret_cast<const uint4 *>(row + 16 * xswz(c0 + i));
+                buf[4 * i + 0] = v.x;
+                if (4 * i + 1 < ne) buf[4 * i + 1] = v.y;
+                if (4 * i + 2 < ne) buf[4 * i + 2] = v.z;
+                if (4 * i + 3 < ne) buf[4 * i + 3] = v.w;
+            }
         }
-        static_for<0, S>([&](auto r_) {
-            constexpr int r = decltype(r_)::value;
-            constexpr int off = lk(K, r, a);
+    };
+    if constexpr (S == 1) {
+        uint32_t b0[R];
+        load(0, R, b0);
 #pragma unroll
-            for (int j = 0; j < R; ++j) acc[r][j] = acc[r][j] + Lane<Acc>::get(buf[j + off]);
+        for (int j = 0; j < R; ++j) acc[0][j] = acc[0][j] + Lane<Acc>::get(b0[j]);
+    } else {
+        static_for<0, S / 2>([&](auto p_) {
+            constexpr int a0 = 2 * decltype(p_)::value, a1 = a0 + 1;
+            uint32_t b0[R + a0], b1[R + a1];
+            load(a0, R + a0, b0);
+            load(a1, R + a1, b1);
+            static_for<0, S>([&](auto r_) {
+                constexpr int r = decltype(r_)::value;
+                constexpr int o0 = lk(K, r, a0), o1 = lk(K, r, a1);
+                constexpr bool fma = (r % 8) < 3;
+#pragma unroll
+                for (int j = 0; j < R; ++j) acc[r][j] = add2<Acc>(acc[r][j], b0[j + o0], b1[j + o1], one, fma);
+            });
         });
-    });
+    }
+}
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool valid) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gmem), "r"(valid ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+// NW output words starting `b` bytes (0..15) into the window w[0 .. NW + 3].
+template <int NW>
+__device__ __forceinline__ void realign_words(const uint32_t *w, int b, uint32_t *o) {
+    const int ws = b >> 2, bs = (b & 3) * 8;
+    uint32_t t[NW + 2], u[NW + 1];
+#pragma unroll
+    for (int i = 0; i < NW + 2; ++i) t[i] = (ws & 2) ? w[i + 2] : w[i];
+#pragma unroll
+    for (int i = 0; i < NW + 1; ++i) u[i] = (ws & 1) ? t[i + 1] : t[i];
+#pragma unroll
+    for (int i = 0; i < NW; ++i) o[i] = __funnelshift_r(u[i], u[i + 1], bs);
 }
 
 template <int K, int R, int T, class In, class Acc, class Out, bool FIRST, bool FINAL>
-__global__ void __launch_bounds__(DrtGeom<K, R, T>::THREADS)
+__global__ void __maxnreg__((DrtGeom<K, R, T, !FIRST && sizeof(In) == 2>::MAXREG))
 drt_pass_kernel(const DrtPass p) {
-    using G = DrtGeom<K, R, T>;
-    constexpr int S = G::S, PI = G::PI, WIN = G::WIN;
-    extern __shared__ uint4 smem_u4[];
-    uint32_t *sm = reinterpret_cast<uint32_t *>(smem_u4);
+    constexpr bool STAGE16 = !FIRST && sizeof(In) == 2;
+    using G = DrtGeom<K, R, T, STAGE16>;
+    constexpr int S = G::S, SP = G::SP, BW = G::BW;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    unsigned char *sm = smem_raw;
 
     const int tid = threadIdx.x;
     const int tile = blockIdx.x, g = blockIdx.y, li = blockIdx.z;
@@ -119,35 +190,29 @@ drt_pass_kernel(const DrtPass p) {
     const int N = p.N;
     const int cK = c + K;
 
-    // ---- output addressing
-    auto out_row_index = [&](int r1, int r2) -> long long {
-        const int s1 = (sg1 << K) + r1, s2 = (sg2 << K) + r2;
-        return ((((long long)s1 << cK) + s2) << (2 * m)) + ((long long)V1 << m) + V2;
-    };
+    // ---- output addressing: row (r1, r2) = row0(r1) + r2 * 2^(2m)
     Out *outp = reinterpret_cast<Out *>(p.out);
     const long long out_inst = FINAL ? (long long)inst * p.out_inst_stride : (long long)li * p.out_inst_stride;
-
+    const long long r2_stride = (long long)p.out_pitch << (2 * m);
+    auto row_ptr = [&](int r1) -> Out * {
+        const long long s1 = (sg1 << K) + r1, s2 = (long long)sg2 << K;
+        const long long row = (((s1 << cK) + s2) << (2 * m)) + ((long long)V1 << m) + V2;
+        return outp + out_inst + row * p.out_pitch + d0;
+    };
     // mosaic placement of a final row (Alg. 2 OutOrder / DodecantCoords)
-    const int mos_b = inst / p.ndod, mos_j = inst - mos_b * p.ndod;
-    auto mosaic_row = [&](int r1, int r2) -> long long {
-        const int b = mos_b, j = mos_j;
+    auto store_mosaic = [&](int r1, int r2, int e, Acc v) {
+        const int D = d0 + e;
+        if (D < 2 || D >= p.out_width) return;
+        const int b = inst / p.ndod, j = inst - b * p.ndod;
         const int s[2] = {(sg1 << K) + r1, (sg2 << K) + r2};
         const int o0 = p.out_order[j][0], o1 = p.out_order[j][1];
         int w0 = s[(o0 < 0 ? -o0 : o0) - 1], w1 = s[(o1 < 0 ? -o1 : o1) - 1];
         if (o0 < 0) w0 = N - 1 - w0;
         if (o1 < 0) w1 = N - 1 - w1;
         const long long rr = (long long)(p.coords[j][0] * N + w0) * (4 * N) + (p.coords[j][1] * N + w1);
-        return (long long)b * 16 * N * N * (3 * N - 2) + rr * (3 * N - 2);
+        outp[(long long)b * 16 * N * N * (3 * N - 2) + rr * (3 * N - 2) + D - 2] = to_out<Out, Acc>(v);
     };
-    auto store_scalar = [&](int r1, int r2, int e, Acc v) {
-        const int D = d0 + e;
-        if (D >= p.out_width) return;
-        if (FINAL && p.layout == 1) {
-            if (D >= 2) outp[mosaic_row(r1, r2) + D - 2] = to_out<Out, Acc>(v);
-        } else {
-            outp[out_inst + out_row_index(r1, r2) * p.out_pitch + D] = to_out<Out, Acc>(v);
-        }
-    };
+    const bool mosaic = FINAL && p.layout == 1;
 
     // ---- tiles entirely outside the support of all 4^K output rows: zeros
     // (support D >= 2N - s1 - s2)
@@ -155,45 +220,41 @@ drt_pass_kernel(const DrtPass p) {
         const int s1max = (sg1 << K) + S - 1, s2max = (sg2 << K) + S - 1;
         if (Dabs + T <= 2 * N - s1max - s2max) {
             constexpr int EPV = 16 / (int)sizeof(Out);
-            const bool vz = (!FINAL || p.layout == 0) && ((p.out_pitch * (int)sizeof(Out)) % 16 == 0) &&
+            const bool vz = !mosaic && ((p.out_pitch * (int)sizeof(Out)) % 16 == 0) &&
                             ((d0 * (int)sizeof(Out)) % 16 == 0) && (d0 + T <= p.out_width);
             if (vz) {
                 for (int i = tid; i < S * S * (T / EPV); i += blockDim.x) {
                     const int rr = i / (T / EPV), q = i - rr * (T / EPV);
-                    Out *dst = outp + out_inst + out_row_index(rr / S, rr % S) * p.out_pitch + d0 + q * EPV;
-                    *reinterpret_cast<uint4 *>(dst) = make_uint4(0u, 0u, 0u, 0u);
+                    Out *dst = row_ptr(rr / S) + (rr % S) * r2_stride + q * EPV;
+                    if (FINAL) st_cs_v4(dst, 0u, 0u, 0u, 0u);
+                    else *reinterpret_cast<uint4 *>(dst) = make_uint4(0u, 0u, 0u, 0u);
                 }
             } else {
                 for (int i = tid; i < S * S * T; i += blockDim.x) {
                     const int rr = i / T, e = i - rr * T;
-                    store_scalar(rr / S, rr % S, e, Acc(0));
+                    if (mosaic) store_mosaic(rr / S, rr % S, e, Acc(0));
+                    else if (d0 + e < p.out_width) row_ptr(rr / S)[(rr % S) * r2_stride + e] = to_out<Out, Acc>(Acc(0));
                 }
             }
             return;
         }
     }
 
-    // ---- stage the 4^K input rows of the group into shared memory
+    // ---- stage the 4^K input rows of the group (32-bit lanes, BW elements per slot)
     auto put = [&](int slot, int e, uint32_t bits) {
-        sm[slot * PI + (((e >> 2) ^ swz<K>(slot)) << 2) + (e & 3)] = bits;
+        *reinterpret_cast<uint32_t *>(sm + slot * SP + 16 * xswz(e >> 2) + 4 * (e & 3)) = bits;
+    };
+    auto put4 = [&](int slot, int chunk, uint4 v) {
+        *reinterpret_cast<uint4 *>(sm + slot * SP + 16 * xswz(chunk)) = v;
     };
     if constexpr (FIRST) {
         const Orient o = p.ori[inst % p.ndod];
         const In *cube = reinterpret_cast<const In *>(p.in) + (long long)(inst / p.ndod) * N * N * N;
         const int z0 = Dabs - 2 * N;       // z' of element 0 (stage-0 rows: D = z' + 2N)
         const int xb = V1 << K, yb = V2 << K;
-        if (!p.vec_ok) {
-            for (int i = tid; i < S * S * WIN; i += blockDim.x) {
-                const int e = i % WIN, slot = i / WIN;
-                const int w1 = slot / S, w2 = slot % S, z = z0 + e;
-                uint32_t bits = 0;
-                if ((unsigned)z < (unsigned)N)
-                    bits = Elem<In>::load_bits(cube + o.off0 + (xb + w1) * o.sx + (yb + w2) * o.sy + z * o.sz);
-                put(slot, e, bits);
-            }
-        } else if (sizeof(In) == 1 && o.fast == 2 && o.sz > 0 && (z0 & 15) == 0 && 16 * ((WIN + 15) / 16) <= PI) {
+        if (sizeof(In) == 1 && p.vec_ok && o.fast == 2 && o.sz > 0 && (z0 & 15) == 0) {
             // u8 rows along z' (forward, 16-aligned): one LDG.128 = 16 voxels = 4 SMEM chunks
-            constexpr int NQ16 = (WIN + 15) / 16;
+            constexpr int NQ16 = BW / 16;
             constexpr int ITEMS = 4;
             for (int base = tid; base < S * S * NQ16; base += blockDim.x * ITEMS) {
                 uint4 v[ITEMS];
@@ -217,29 +278,27 @@ drt_pass_kernel(const DrtPass p) {
                 for (int u = 0; u < ITEMS; ++u) {
                     if (sl[u] < 0) continue;
                     const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-                    const int sw = swz<K>(sl[u]);
 #pragma unroll
-                    for (int h = 0; h < 4; ++h) {
-                        const uint4 o4 = make_uint4(__byte_perm(w[h], 0, 0x4440), __byte_perm(w[h], 0, 0x4441),
-                                                    __byte_perm(w[h], 0, 0x4442), __byte_perm(w[h], 0, 0x4443));
-                        *reinterpret_cast<uint4 *>(sm + sl[u] * PI + (((4 * qq[u] + h) ^ sw) << 2)) = o4;
-                    }
+                    for (int h = 0; h < 4; ++h)
+                        put4(sl[u], 4 * qq[u] + h,
+                             make_uint4(__byte_perm(w[h], 0, 0x4440), __byte_perm(w[h], 0, 0x4441),
+                                        __byte_perm(w[h], 0, 0x4442), __byte_perm(w[h], 0, 0x4443)));
                 }
             }
-        } else if (sizeof(In) == 1 && K == 4 && o.fast != 2) {
+        } else if (sizeof(In) == 1 && K == 4 && p.vec_ok && o.fast != 2) {
             // u8, unit stride along x' (fast 0) or y' (fast 1): one LDG.128 = the 16 voxels of a
             // run along that axis; 4 consecutive z' per item are transposed in registers so every
             // SMEM write is a 16-byte chunk (4 consecutive e of one slot)
             const bool fx = o.fast == 0;
             const long long sf = fx ? o.sx : o.sy, so = fx ? o.sy : o.sx;
             const int fb = fx ? xb : yb, ob = fx ? yb : xb;
-            constexpr int NG = (WIN + 3) / 4;
+            constexpr int NG = BW / 4;
             for (int it = tid; it < S * NG; it += blockDim.x) {
-                const int other = it % S, g = it / S;
+                const int other = it % S, gq = it / S;
                 uint4 v[4];
 #pragma unroll
                 for (int t = 0; t < 4; ++t) {
-                    const int z = z0 + 4 * g + t;
+                    const int z = z0 + 4 * gq + t;
                     v[t] = make_uint4(0u, 0u, 0u, 0u);
                     if ((unsigned)z < (unsigned)N) {
                         const long long b = o.off0 + (long long)(ob + other) * so + (long long)z * o.sz +
@@ -249,416 +308,221 @@ drt_pass_kernel(const DrtPass p) {
                 }
 #pragma unroll
                 for (int wf = 0; wf < 16; ++wf) {
-                    const int byte = sf > 0 ? wf : 15 - wf;     // runtime-uniform direction
+                    const int byte = sf > 0 ? wf : 15 - wf;
                     uint32_t q4[4];
 #pragma unroll
                     for (int t = 0; t < 4; ++t) {
                         const uint32_t w[4] = {v[t].x, v[t].y, v[t].z, v[t].w};
                         q4[t] = __byte_perm(w[byte >> 2], 0, 0x4440 | (byte & 3));
                     }
-                    const int slot = fx ? wf * S + other : other * S + wf;
-                    *reinterpret_cast<uint4 *>(sm + slot * PI + ((g ^ swz<K>(slot)) << 2)) =
-                        make_uint4(q4[0], q4[1], q4[2], q4[3]);
+                    put4(fx ? wf * S + other : other * S + wf, gq, make_uint4(q4[0], q4[1], q4[2], q4[3]));
                 }
             }
-        } else if (o.fast == 2) {
-            // rows along z' are contiguous in the original cube (reversed when sz < 0)
-            stage_rows<In, 8>(S * S, WIN, [&](int slot) {
-                const int w1 = slot / S, w2 = slot % S;
-                const long long b = o.off0 + (long long)(xb + w1) * o.sx + (long long)(yb + w2) * o.sy;
-                RowSrc<In> r;
-                if (o.sz > 0) { r.ptr = cube + b; r.st = z0; r.dir = 1; }
-                else { r.ptr = cube + b - (N - 1); r.st = N - 1 - z0; r.dir = -1; }
-                r.width = N;
-                return r;
-            }, put);
         } else {
-            // the unit-stride axis is x' (fast 0) or y' (fast 1): stage runs of S voxels along it
-            const bool fx = o.fast == 0;
-            stage_rows<In, 8>(S * WIN, S, [&](int r) {
-                const int other = r % S, e = r / S, z = z0 + e;
-                const long long sf = fx ? o.sx : o.sy, so = fx ? o.sy : o.sx;
-                const int fb = fx ? xb : yb, ob = fx ? yb : xb;
-                const long long b = o.off0 + (long long)(ob + other) * so + (long long)z * o.sz;
-                RowSrc<In> rr;
-                if (sf > 0) { rr.ptr = cube + b; rr.st = fb; rr.dir = 1; }
-                else { rr.ptr = cube + b - (N - 1); rr.st = N - 1 - fb; rr.dir = -1; }
-                rr.width = ((unsigned)z < (unsigned)N) ? N : 0;
-                return rr;
-            }, [&](int r, int wf, uint32_t bits) {
-                const int other = r % S, e = r / S;
-                put(fx ? wf * S + other : other * S + wf, e, bits);
-            });
+            // generic (any voxel type, any orientation, small N): element by element
+            for (int i = tid; i < S * S * BW; i += blockDim.x) {
+                const int e = i % BW, slot = i / BW;
+                const int w1 = slot / S, w2 = slot % S, z = z0 + e;
+                uint32_t bits = 0;
+                if ((unsigned)z < (unsigned)N)
+                    bits = Elem<In>::load_bits(cube + o.off0 + (long long)(xb + w1) * o.sx +
+                                               (long long)(yb + w2) * o.sy + (long long)z * o.sz);
+                put(slot, e, bits);
+            }
         }
-    } else {
+    } else if constexpr (STAGE16) {
+        // u16 stage-c rows.  Phase 1: cp.async the NRAW aligned 16-byte source chunks that cover
+        // the slot's range [st, st + BW) (st = tile origin + pre-shift s1 w1 + s2 w2) into the
+        // slot's raw area -- asynchronous, no registers, out-of-row chunks zero-filled.  Phase 2:
+        // realign each slot by its runtime byte offset into the staged u16 row.
         const In *inb = reinterpret_cast<const In *>(p.in) + (long long)li * p.in_inst_stride;
         const int nc = p.n - c;
         const long long rbase = (((long long)sg1 << c) + sg2) << (2 * nc);
-        stage_rows<In, 8>(S * S, WIN, [&](int slot) {
-            const int w1 = slot / S, w2 = slot % S;
+        const int nchunk = p.in_width >> 3;                 // chunks per stored row (width = pitch)
+        constexpr int NRAW = G::NRAW, HALF = (NRAW + 1) / 2;
+        for (int it = tid; it < S * S * 2; it += blockDim.x) {
+            const int slot = it >> 1, h = it & 1;
+            const int w1 = slot >> K, w2 = slot & (S - 1);
             const long long row = rbase + ((long long)((V1 << K) + w1) << nc) + (V2 << K) + w2;
-            RowSrc<In> r;
-            r.ptr = inb + row * p.in_pitch;
-            r.st = Dabs + sg1 * w1 + sg2 * w2 - p.in_base;
-            r.dir = 1;
-            r.width = p.in_width;
-            return r;
-        }, put);
-    }
-    __syncthreads();
-
-    // ---- x-step: X(r1, w2, j) = sum_w1 staged(w1, w2, j + l^K_{r1}(w1)), kept in registers,
-    // then written in place over the staged rows (slot (r1, w2)).
-    Acc acc[S][R];
-    const bool xact = tid < G::XT;
-    const int xb2 = tid & (S - 1), xr = tid >> K;
-    if (xact) {
+            const int st = Dabs + sg1 * w1 + sg2 * w2 - p.in_base;
+            const int c0 = st >> 3;
+            const uint4 *src = reinterpret_cast<const uint4 *>(inb + row * p.in_pitch);
+            unsigned char *raw = sm + slot * SP + G::RAWOFF;
 #pragma unroll
-        for (int r = 0; r < S; ++r)
-#pragma unroll
-            for (int j = 0; j < R; ++j) acc[r][j] = Acc(0);
-        drt_direct_sum<K, R, PI, Acc>(sm, xb2, S, xr * (R / 4), acc);
-    }
-    __syncthreads();
-    if (xact) {
-#pragma unroll
-        for (int r = 0; r < S; ++r) {
-            const int slot = r * S + xb2;
-            const int sw = swz<K>(slot);
-#pragma unroll
-            for (int q = 0; q < R / 4; ++q) {
-                uint4 v;
-                v.x = Lane<Acc>::bits(acc[r][4 * q + 0]);
-                v.y = Lane<Acc>::bits(acc[r][4 * q + 1]);
-                v.z = Lane<Acc>::bits(acc[r][4 * q + 2]);
-                v.w = Lane<Acc>::bits(acc[r][4 * q + 3]);
-                *reinterpret_cast<uint4 *>(sm + slot * PI + (((xr * (R / 4) + q) ^ sw) << 2)) = v;
-            }
-        }
-    }
-    __syncthreads();
-
-    // ---- y-step: out(r1, r2, j) = sum_w2 X(r1, w2, j + l^K_{r2}(w2)); store
-    if (tid < G::YT) {
-        const int r1 = tid & (S - 1), yr = tid >> K;
-#pragma unroll
-        for (int r = 0; r < S; ++r)
-#pragma unroll
-            for (int j = 0; j < R; ++j) acc[r][j] = Acc(0);
-        drt_direct_sum<K, R, PI, Acc>(sm, r1 * S, 1, yr * (R / 4), acc);
-
-        const int e0 = yr * R;
-        const bool vec_ok = (!FINAL || p.layout == 0) && (d0 + e0 + R <= p.out_width) &&
-                            ((p.out_pitch * (int)sizeof(Out)) % 16 == 0) && (((d0 + e0) * (int)sizeof(Out)) % 16 == 0);
-#pragma unroll
-        for (int r2 = 0; r2 < S; ++r2) {
-            if (vec_ok) {
-                Out *dst = outp + out_inst + out_row_index(r1, r2) * p.out_pitch + d0 + e0;
-                if constexpr (sizeof(Out) == 2) {
-#pragma unroll
-                    for (int q = 0; q < R / 8; ++q) {
-                        uint32_t w[4];
-#pragma unroll
-                        for (int h = 0; h < 4; ++h)
-                            w[h] = (uint32_t)to_out<Out, Acc>(acc[r2][8 * q + 2 * h]) |
-                                   ((uint32_t)to_out<Out, Acc>(acc[r2][8 * q + 2 * h + 1]) << 16);
-                        *reinterpret_cast<uint4 *>(dst + 8 * q) = make_uint4(w[0], w[1], w[2], w[3]);
-                    }
-                } else {
-#pragma unroll
-                    for (int q = 0; q < R / 4; ++q) {
-                        const uint32_t a0 = Lane<Acc>::bits(acc[r2][4 * q + 0]), a1 = Lane<Acc>::bits(acc[r2][4 * q + 1]);
-                        const uint32_t a2 = Lane<Acc>::bits(acc[r2][4 * q + 2]), a3 = Lane<Acc>::bits(acc[r2][4 * q + 3]);
-                        if (FINAL) st_cs_v4(dst + 4 * q, a0, a1, a2, a3);
-                        else *reinterpret_cast<uint4 *>(dst + 4 * q) = make_uint4(a0, a1, a2, a3);
-                    }
+            for (int k = 0; k < HALF; ++k) {
+                const int kk = h * HALF + k;
+                if (kk < NRAW) {
+                    const int cc = c0 + kk;
+                    const bool ok = (unsigned)cc < (unsigned)nchunk;
+                    cp_async16(raw + 16 * kk, ok ? (const void *)(src + cc) : (const void *)inb, ok);
                 }
-            } else {
-#pragma unroll
-                for (int j = 0; j < R; ++j) store_scalar(r1, r2, e0 + j, acc[r2][j]);
             }
         }
-    }
-}
-
-
-// ===========================================================================
-// Non-first passes.  The 4^K stage-c rows are staged in their storage type
-// (u16 or 32-bit): each 16-byte SMEM chunk is built from two aligned 16-byte
-// global loads and an in-register realignment by the row's runtime
-// displacement (sigma1 w1 + sigma2 w2 is arbitrary, so neither TMA nor plain
-// vector loads can place it directly).  X is written in place as 32-bit lanes
-// with an XOR swizzle; sums use 3-input adds.
-// ===========================================================================
-template <int K, int R, int T, class MidIn>
-struct DrtMidGeom {
-    static constexpr int S = 1 << K;
-    static constexpr int H = S - 1;
-    static constexpr int WIN = T + 2 * H;
-    static constexpr int EPC = 16 / (int)sizeof(MidIn);            // elements per 16-byte chunk
-    static constexpr int NRX = (T + H + R - 1) / R;
-    static constexpr int NRY = T / R;
-    static constexpr int RD = (NRX - 1) * R + (R + H + EPC - 1) / EPC * EPC;   // input elements touched
-    static constexpr int BOXW = ((WIN > RD ? WIN : RD) + EPC - 1) / EPC * EPC;  // staged elements per row
-    static constexpr int NQ = BOXW / EPC;                           // staged chunks per row
-    static constexpr int XW = ((NRX * R + 31) / 32) * 32;           // X words per slot (8-chunk groups)
-    static constexpr int SLOT_IN = BOXW * (int)sizeof(MidIn);
-    static constexpr int SP0 = (((SLOT_IN > XW * 4) ? SLOT_IN : XW * 4) + 15) / 16 * 16;
-    static constexpr int SP = (SP0 % 128 == 0) ? SP0 + 16 : SP0;    // slot pitch (bytes), rotates banks across slots
-    static constexpr int XT = S * NRX;
-    static constexpr int YT = S * NRY;
-    static constexpr int THREADS = ((XT > YT ? XT : YT) + 31) / 32 * 32;
-    static constexpr int SMEM = S * S * SP;
-    // two CTAs per SM: with W warps per CTA an SM sub-partition holds ceil(2W/4) warps of its
-    // 16K-register file, which caps the registers per thread
-    static constexpr int WARPS = THREADS / 32;
-    static constexpr int MAXREG0 = 16384 / (((2 * WARPS + 3) / 4) * 32) / 8 * 8;
-    static constexpr int MAXREG = MAXREG0 > 255 ? 255 : MAXREG0;
-    static_assert(T % R == 0 && R % 4 == 0 && (R % EPC == 0 || EPC > R), "tile shape");
-    static_assert((NRY - 1) * R + (R + H + 3) / 4 * 4 <= NRX * R, "y-step reads inside X");
-};
-
-// 16 bytes starting `b` bytes (0..15) into the 32-byte window lo:hi.
-__device__ __forceinline__ uint4 realign16(const uint4 &lo, const uint4 &hi, int b) {
-    const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-    const int ws = b >> 2, bs = (b & 3) * 8;
-    uint32_t t[6], u[5];
+        cp_async_wait_all();
+        __syncthreads();
+        constexpr int NQS = BW / 8;
+        constexpr int PQ = NQS % 6 == 0 ? 6 : (NQS % 4 == 0 ? 4 : (NQS % 3 == 0 ? 3 : 2));
+        constexpr int NPART = NQS / PQ;
+        static_assert(NQS % PQ == 0, "staging split");
+        for (int it = tid; it < S * S * NPART; it += blockDim.x) {
+            const int slot = it / NPART, part = it - slot * NPART;
+            const int w1 = slot >> K, w2 = slot & (S - 1);
+            const int bsh = ((Dabs + sg1 * w1 + sg2 * w2 - p.in_base) & 7) * 2;
+            const unsigned char *raw = sm + slot * SP + G::RAWOFF + 16 * part * PQ;
+            uint32_t w[4 * (PQ + 1)];
 #pragma unroll
-    for (int i = 0; i < 6; ++i) t[i] = (ws & 2) ? w[i + 2] : w[i];
+            for (int k = 0; k <= PQ; ++k) {
+                const uint4 v = *reinterpret_cast<const uint4 *>(raw + 16 * k);
+                w[4 * k + 0] = v.x;
+                w[4 * k + 1] = v.y;
+                w[4 * k + 2] = v.z;
+                w[4 * k + 3] = v.w;
+            }
+            uint32_t o[4 * PQ];
+            realign_words<4 * PQ>(w, bsh, o);
 #pragma unroll
-    for (int i = 0; i < 5; ++i) u[i] = (ws & 1) ? t[i + 1] : t[i];
-    uint4 o;
-    o.x = __funnelshift_r(u[0], u[1], bs);
-    o.y = __funnelshift_r(u[1], u[2], bs);
-    o.z = __funnelshift_r(u[2], u[3], bs);
-    o.w = __funnelshift_r(u[3], u[4], bs);
-    return o;
-}
-
-__device__ __forceinline__ int xswz(int c) { return c ^ ((c >> 3) & 1); }
-
-// Load elements [0, NE) of a row starting at `row` (run-aligned), unpacked to 32-bit lanes.
-template <class MidIn, int NE>
-__device__ __forceinline__ void load_run(const unsigned char *row, uint32_t *buf) {
-    if constexpr (sizeof(MidIn) == 2) {
-#pragma unroll
-        for (int i = 0; i < (NE + 7) / 8; ++i) {
-            const uint4 v = *reinterpret_cast<const uint4 *>(row + 16 * i);
-            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                if (8 * i + q < NE) buf[8 * i + q] = (q & 1) ? (w[q >> 1] >> 16) : (w[q >> 1] & 0xFFFFu);
+            for (int k = 0; k < PQ; ++k)
+                *reinterpret_cast<uint4 *>(sm + slot * SP + 16 * (part * PQ + k)) =
+                    make_uint4(o[4 * k], o[4 * k + 1], o[4 * k + 2], o[4 * k + 3]);
         }
     } else {
-#pragma unroll
-        for (int i = 0; i < (NE + 3) / 4; ++i) {
-            const uint4 v = *reinterpret_cast<const uint4 *>(row + 16 * i);
-            buf[4 * i + 0] = v.x;
-            if (4 * i + 1 < NE) buf[4 * i + 1] = v.y;
-            if (4 * i + 2 < NE) buf[4 * i + 2] = v.z;
-            if (4 * i + 3 < NE) buf[4 * i + 3] = v.w;
-        }
-    }
-}
-
-// acc[r][j] += sum_a row_a[j + l^K_r(a)]; rows taken two at a time so that the
-// integer sums become 3-input adds.  LoadRow(integral_constant a, buf) fills
-// buf[0, R + a) with the row's run.
-template <int K, int R, class Acc, class LoadRow>
-__device__ __forceinline__ void direct_sum2(LoadRow &&load_row, Acc (&acc)[1 << K][R]) {
-    constexpr int S = 1 << K;
-    if constexpr (S == 1) {
-        uint32_t b0[R];
-        load_row(std::integral_constant<int, 0>{}, b0);
-#pragma unroll
-        for (int j = 0; j < R; ++j) acc[0][j] = acc[0][j] + Lane<Acc>::get(b0[j]);
-    } else {
-        static_for<0, S / 2>([&](auto p_) {
-            constexpr int a0 = 2 * decltype(p_)::value, a1 = a0 + 1;
-            uint32_t b0[R + a0], b1[R + a1];
-            load_row(std::integral_constant<int, a0>{}, b0);
-            load_row(std::integral_constant<int, a1>{}, b1);
-            static_for<0, S>([&](auto r_) {
-                constexpr int r = decltype(r_)::value;
-                constexpr int o0 = lk(K, r, a0), o1 = lk(K, r, a1);
-#pragma unroll
-                for (int j = 0; j < R; ++j)
-                    acc[r][j] = acc[r][j] + Lane<Acc>::get(b0[j + o0]) + Lane<Acc>::get(b1[j + o1]);
-            });
-        });
-    }
-}
-
-template <int K, int R, int T, class MidIn, class Acc, class Out, bool FINAL>
-__global__ void __maxnreg__((DrtMidGeom<K, R, T, MidIn>::MAXREG))
-drt_pass_mid_kernel(const DrtPass p) {
-    using G = DrtMidGeom<K, R, T, MidIn>;
-    constexpr int S = G::S, SP = G::SP, EPC = G::EPC, NQ = G::NQ;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    unsigned char *sm = smem_raw;
-
-    const int tid = threadIdx.x;
-    const int tile = blockIdx.x, g = blockIdx.y, li = blockIdx.z;
-    const int inst = p.inst0 + li;
-    const int m = p.m, c = p.c, N = p.N, cK = c + K;
-    const int V2 = g & ((1 << m) - 1);
-    const int V1 = (g >> m) & ((1 << m) - 1);
-    const int sig = g >> (2 * m);
-    const int sg2 = sig & ((1 << c) - 1);
-    const int sg1 = sig >> c;
-    const int d0 = tile * T;
-    const int Dabs = p.out_base + d0;
-
-    auto out_row_index = [&](int r1, int r2) -> long long {
-        const int s1 = (sg1 << K) + r1, s2 = (sg2 << K) + r2;
-        return ((((long long)s1 << cK) + s2) << (2 * m)) + ((long long)V1 << m) + V2;
-    };
-    Out *outp = reinterpret_cast<Out *>(p.out);
-    const long long out_inst = FINAL ? (long long)inst * p.out_inst_stride : (long long)li * p.out_inst_stride;
-    const int mos_b = inst / p.ndod, mos_j = inst - mos_b * p.ndod;
-    auto mosaic_row = [&](int r1, int r2) -> long long {
-        const int b = mos_b, j = mos_j;
-        const int s[2] = {(sg1 << K) + r1, (sg2 << K) + r2};
-        const int o0 = p.out_order[j][0], o1 = p.out_order[j][1];
-        int w0 = s[(o0 < 0 ? -o0 : o0) - 1], w1 = s[(o1 < 0 ? -o1 : o1) - 1];
-        if (o0 < 0) w0 = N - 1 - w0;
-        if (o1 < 0) w1 = N - 1 - w1;
-        const long long rr = (long long)(p.coords[j][0] * N + w0) * (4 * N) + (p.coords[j][1] * N + w1);
-        return (long long)b * 16 * N * N * (3 * N - 2) + rr * (3 * N - 2);
-    };
-    auto store_scalar = [&](int r1, int r2, int e, Acc v) {
-        const int D = d0 + e;
-        if (D >= p.out_width) return;
-        if (FINAL && p.layout == 1) {
-            if (D >= 2) outp[mosaic_row(r1, r2) + D - 2] = to_out<Out, Acc>(v);
-        } else {
-            outp[out_inst + out_row_index(r1, r2) * p.out_pitch + D] = to_out<Out, Acc>(v);
-        }
-    };
-
-    // ---- zero tiles (support D >= 2N - s1 - s2)
-    {
-        const int s1max = (sg1 << K) + S - 1, s2max = (sg2 << K) + S - 1;
-        if (Dabs + T <= 2 * N - s1max - s2max) {
-            constexpr int EPV = 16 / (int)sizeof(Out);
-            const bool vz = (!FINAL || p.layout == 0) && ((p.out_pitch * (int)sizeof(Out)) % 16 == 0) &&
-                            ((d0 * (int)sizeof(Out)) % 16 == 0) && (d0 + T <= p.out_width);
-            if (vz) {
-                for (int i = tid; i < S * S * (T / EPV); i += blockDim.x) {
-                    const int rr = i / (T / EPV), q = i - rr * (T / EPV);
-                    Out *dst = outp + out_inst + out_row_index(rr / S, rr % S) * p.out_pitch + d0 + q * EPV;
-                    if (FINAL) st_cs_v4(dst, 0u, 0u, 0u, 0u);
-                    else *reinterpret_cast<uint4 *>(dst) = make_uint4(0u, 0u, 0u, 0u);
-                }
-            } else {
-                for (int i = tid; i < S * S * T; i += blockDim.x) {
-                    const int rr = i / T, e = i - rr * T;
-                    store_scalar(rr / S, rr % S, e, Acc(0));
-                }
-            }
-            return;
-        }
-    }
-
-    // ---- stage: SMEM chunk q of slot (w1, w2) = elements [st + EPC q, st + EPC (q+1)) of the
-    // stage-c row, st = displacement of the row (its pre-shift); out-of-row chunks read as 0
-    // (the stored rows are zero-padded up to their pitch).
-    {
-        const MidIn *inb = reinterpret_cast<const MidIn *>(p.in) + (long long)li * p.in_inst_stride;
+        // stage-c rows: the slot's staged element e is stored element st + e of its row, st =
+        // tile origin + pre-shift s1 w1 + s2 w2.  Aligned 16-byte loads of PQ+1 consecutive chunks
+        // are realigned in registers to the row's runtime byte offset, then widened to 32 bits.
+        constexpr int EPC = 16 / (int)sizeof(In);         // source elements per 16-byte chunk
+        constexpr int LOG_EPC = EPC == 8 ? 3 : 2;
+        constexpr int NQS = BW / EPC;                      // source chunks per slot
+        constexpr int PQ = NQS % 6 == 0 ? 6 : (NQS % 4 == 0 ? 4 : (NQS % 3 == 0 ? 3 : 2));
+        constexpr int NPART = NQS / PQ;
+        static_assert(NQS % PQ == 0, "staging split");
+        const In *inb = reinterpret_cast<const In *>(p.in) + (long long)li * p.in_inst_stride;
         const int nc = p.n - c;
         const long long rbase = (((long long)sg1 << c) + sg2) << (2 * nc);
-        const int nchunk = p.in_width / EPC;                 // chunks per stored row (width = pitch)
-        constexpr int ITEMS = 4;
-        for (int base = tid; base < S * S * NQ; base += blockDim.x * ITEMS) {
-            uint4 lo[ITEMS], hi[ITEMS];
-            int bsh[ITEMS], dst[ITEMS];
+        const int nchunk = p.in_width >> LOG_EPC;          // chunks per stored row (width = pitch)
+        constexpr int ITEMS = 2;                           // items whose loads are in flight together
+        for (int base = tid; base < S * S * NPART; base += blockDim.x * ITEMS) {
+            uint32_t w[ITEMS][4 * (PQ + 1)];
+            int bsh[ITEMS], slot_[ITEMS], part_[ITEMS];
 #pragma unroll
             for (int u = 0; u < ITEMS; ++u) {
                 const int it = base + u * blockDim.x;
-                dst[u] = -1;
-                lo[u] = hi[u] = make_uint4(0u, 0u, 0u, 0u);
-                if (it < S * S * NQ) {
-                    const int slot = it / NQ, q = it - slot * NQ;
-                    const int w1 = slot / S, w2 = slot - w1 * S;
+                slot_[u] = -1;
+                bsh[u] = 0;
+                int c0 = -1 << 20;
+                const uint4 *src = nullptr;
+                if (it < S * S * NPART) {
+                    const int slot = it / NPART, part = it - slot * NPART;
+                    const int w1 = slot >> K, w2 = slot & (S - 1);
                     const long long row = rbase + ((long long)((V1 << K) + w1) << nc) + (V2 << K) + w2;
-                    const int e0 = Dabs + sg1 * w1 + sg2 * w2 - p.in_base + EPC * q;
-                    const int c0 = floor_div(e0, EPC);
-                    bsh[u] = (e0 - c0 * EPC) * (int)sizeof(MidIn);
-                    dst[u] = slot * SP + 16 * q;
-                    const uint4 *src = reinterpret_cast<const uint4 *>(inb + row * p.in_pitch);
-                    if (c0 >= 0 && c0 < nchunk) lo[u] = __ldg(src + c0);
-                    if (bsh[u] != 0 && c0 + 1 >= 0 && c0 + 1 < nchunk) hi[u] = __ldg(src + c0 + 1);
+                    const int st = Dabs + sg1 * w1 + sg2 * w2 - p.in_base;
+                    c0 = (st >> LOG_EPC) + part * PQ;          // arithmetic shift = floor division
+                    bsh[u] = (st & (EPC - 1)) * (int)sizeof(In);
+                    slot_[u] = slot;
+                    part_[u] = part;
+                    src = reinterpret_cast<const uint4 *>(inb + row * p.in_pitch);
+                }
+#pragma unroll
+                for (int k = 0; k <= PQ; ++k) {
+                    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+                    if ((unsigned)(c0 + k) < (unsigned)nchunk) v = __ldg(src + c0 + k);
+                    w[u][4 * k + 0] = v.x;
+                    w[u][4 * k + 1] = v.y;
+                    w[u][4 * k + 2] = v.z;
+                    w[u][4 * k + 3] = v.w;
                 }
             }
 #pragma unroll
-            for (int u = 0; u < ITEMS; ++u)
-                if (dst[u] >= 0) *reinterpret_cast<uint4 *>(sm + dst[u]) = realign16(lo[u], hi[u], bsh[u]);
+            for (int u = 0; u < ITEMS; ++u) {
+                if (slot_[u] < 0) continue;
+                const int slot = slot_[u], part = part_[u];
+                uint32_t o[4 * PQ];
+                realign_words<4 * PQ>(w[u], bsh[u], o);
+                if constexpr (sizeof(In) == 2) {
+#pragma unroll
+                    for (int k = 0; k < PQ; ++k) {
+                        const int ch = 2 * (part * PQ + k);     // two 32-bit chunks per source chunk
+                        put4(slot, ch, make_uint4(o[4 * k] & 0xFFFFu, o[4 * k] >> 16, o[4 * k + 1] & 0xFFFFu, o[4 * k + 1] >> 16));
+                        put4(slot, ch + 1,
+                             make_uint4(o[4 * k + 2] & 0xFFFFu, o[4 * k + 2] >> 16, o[4 * k + 3] & 0xFFFFu, o[4 * k + 3] >> 16));
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < PQ; ++k)
+                        put4(slot, part * PQ + k, make_uint4(o[4 * k], o[4 * k + 1], o[4 * k + 2], o[4 * k + 3]));
+                }
+            }
         }
     }
     __syncthreads();
 
-    // ---- x-step: thread (w2, run) over rows w1; X kept in registers, then in place
+    // ---- x-step (rows w1 of slot (w1, w2) -> X(r1, w2)), written in place over slot (r1, w2),
+    // then y-step (rows w2 of X slot (r1, w2) -> out(r1, r2)); one code path, two iterations.
     Acc acc[S][R];
-    const bool xact = tid < G::XT;
-    const int xr = tid % G::NRX, xw2 = tid / G::NRX;
-    if (xact) {
+    const int xr = tid % G::NRX, xb = tid / G::NRX;
+    const int yr = tid % G::NRY, yb = tid / G::NRY;
+    auto zero_acc = [&]() {
 #pragma unroll
-        for (int r = 0; r < S; ++r)
+        for (int i = 0; i < S; ++i)
 #pragma unroll
-            for (int j = 0; j < R; ++j) acc[r][j] = Acc(0);
-        const unsigned char *base = sm + xw2 * SP + xr * R * (int)sizeof(MidIn);
-        direct_sum2<K, R, Acc>([&](auto a_, uint32_t *buf) {
-            constexpr int a = decltype(a_)::value;
-            load_run<MidIn, R + a>(base + a * S * SP, buf);
-        }, acc);
-    }
-    __syncthreads();
-    if (xact) {
+            for (int j = 0; j < R; ++j) acc[i][j] = Acc(0);
+    };
+    auto write_x = [&]() {
 #pragma unroll
-        for (int r = 0; r < S; ++r) {
-            unsigned char *slot = sm + (r * S + xw2) * SP;
+        for (int i = 0; i < S; ++i) {
 #pragma unroll
-            for (int q = 0; q < R / 4; ++q) {
-                uint4 v;
-                v.x = Lane<Acc>::bits(acc[r][4 * q + 0]);
-                v.y = Lane<Acc>::bits(acc[r][4 * q + 1]);
-                v.z = Lane<Acc>::bits(acc[r][4 * q + 2]);
-                v.w = Lane<Acc>::bits(acc[r][4 * q + 3]);
-                *reinterpret_cast<uint4 *>(slot + 16 * xswz(xr * (R / 4) + q)) = v;
+            for (int q = 0; q < R / 4; ++q)
+                put4(i * S + xb, xr * (R / 4) + q,
+                     make_uint4(Lane<Acc>::bits(acc[i][4 * q + 0]), Lane<Acc>::bits(acc[i][4 * q + 1]),
+                                Lane<Acc>::bits(acc[i][4 * q + 2]), Lane<Acc>::bits(acc[i][4 * q + 3])));
+        }
+    };
+    if constexpr (STAGE16) {
+        // x-step reads the u16 staged rows, y-step the 32-bit X rows
+        if (tid < G::XT) {
+            zero_acc();
+            drt_accumulate<K, R, SP, true, Acc>(sm, xb, S, xr * (R / 8), p.one, acc);
+        }
+        __syncthreads();
+        if (tid < G::XT) write_x();
+        __syncthreads();
+        if (tid < G::YT) {
+            zero_acc();
+            drt_accumulate<K, R, SP, false, Acc>(sm, yb * S, 1, yr * (R / 4), p.one, acc);
+        }
+    } else {
+        // both steps read 32-bit rows: one code path, two iterations
+#pragma unroll 1
+        for (int step = 0; step < 2; ++step) {
+            const bool act = tid < (step ? G::YT : G::XT);
+            const int r = step ? yr : xr, b = step ? yb : xb;
+            if (act) {
+                zero_acc();
+                drt_accumulate<K, R, SP, false, Acc>(sm, step ? b * S : b, step ? 1 : S, r * (R / 4), p.one, acc);
+            }
+            if (step == 0) {
+                __syncthreads();
+                if (act) write_x();
+                __syncthreads();
             }
         }
     }
-    __syncthreads();
 
-    // ---- y-step: thread (r1, run) over X rows w2; store
+    // ---- store out(r1 = yb, r2, run yr)
     if (tid < G::YT) {
-        const int yr = tid % G::NRY, r1 = tid / G::NRY;
+        const int r1 = yb, e0 = yr * R;
+        if (mosaic) {
 #pragma unroll
-        for (int r = 0; r < S; ++r)
+            for (int r2 = 0; r2 < S; ++r2)
 #pragma unroll
-            for (int j = 0; j < R; ++j) acc[r][j] = Acc(0);
-        const unsigned char *base = sm + (r1 * S) * SP;
-        const int c0 = yr * (R / 4);
-        direct_sum2<K, R, Acc>([&](auto a_, uint32_t *buf) {
-            constexpr int a = decltype(a_)::value;
-            const unsigned char *slot = base + a * SP;
+                for (int j = 0; j < R; ++j) store_mosaic(r1, r2, e0 + j, acc[r2][j]);
+            return;
+        }
+        const bool vec_ok = (d0 + e0 + R <= p.out_width) && ((p.out_pitch * (int)sizeof(Out)) % 16 == 0) &&
+                            (((d0 + e0) * (int)sizeof(Out)) % 16 == 0);
+        Out *dst = row_ptr(r1) + e0;
 #pragma unroll
-            for (int i = 0; i < (R + a + 3) / 4; ++i) {
-                const uint4 v = *reinterpret_cast<const uint4 *>(slot + 16 * xswz(c0 + i));
-                buf[4 * i + 0] = v.x;
-                if (4 * i + 1 < R + a) buf[4 * i + 1] = v.y;
-                if (4 * i + 2 < R + a) buf[4 * i + 2] = v.z;
-                if (4 * i + 3 < R + a) buf[4 * i + 3] = v.w;
-            }
-        }, acc);
-
-        const int e0 = yr * R;
-        const bool vec_ok = (!FINAL || p.layout == 0) && (d0 + e0 + R <= p.out_width) &&
-                            ((p.out_pitch * (int)sizeof(Out)) % 16 == 0) && (((d0 + e0) * (int)sizeof(Out)) % 16 == 0);
-#pragma unroll
-        for (int r2 = 0; r2 < S; ++r2) {
+        for (int r2 = 0; r2 < S; ++r2, dst += r2_stride) {
             if (vec_ok) {
-                Out *dst = outp + out_inst + out_row_index(r1, r2) * p.out_pitch + d0 + e0;
                 if constexpr (sizeof(Out) == 2) {
 #pragma unroll
                     for (int q = 0; q < R / 8; ++q) {
@@ -680,7 +544,8 @@ drt_pass_mid_kernel(const DrtPass p) {
                 }
             } else {
 #pragma unroll
-                for (int j = 0; j < R; ++j) store_scalar(r1, r2, e0 + j, acc[r2][j]);
+                for (int j = 0; j < R; ++j)
+                    if (d0 + e0 + j < p.out_width) dst[j] = to_out<Out, Acc>(acc[r2][j]);
             }
         }
     }

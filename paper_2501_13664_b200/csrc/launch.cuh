@@ -1,42 +1,9 @@
 // launch.cuh -- kernel launch templates (tile shapes per radix) shared by
 // the per-dtype translation units k_*.cu.
 #pragma once
-#include <cudaTypedefs.h>
-
 #include "dispatch.h"
 
 namespace d3 {
-
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
-inline PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
-        void *f = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            f = nullptr;
-        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
-    }();
-    return fn;
-}
-
-// 2D map over `rows` rows of `width` valid elements (row pitch `pitch_elems`),
-// box = `box` elements x 1 row; out-of-bounds reads are zero.
-template <class T>
-bool make_row_tmap(CUtensorMap *m, const void *base, long long rows, int width, int pitch_elems, int box) {
-    auto enc = tmap_encoder();
-    if (!enc) return false;
-    CUtensorMapDataType dt = sizeof(T) == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
-                             : std::is_same<T, float>::value ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
-                                                             : CU_TENSOR_MAP_DATA_TYPE_UINT32;
-    cuuint64_t dims[2] = {(cuuint64_t)width, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)pitch_elems * sizeof(T)};
-    cuuint32_t boxd[2] = {(cuuint32_t)box, 1};
-    cuuint32_t estr[2] = {1, 1};
-    return enc(m, dt, 2, const_cast<void *>(base), dims, strides, boxd, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
 
 template <class KernelT>
 bool set_smem(KernelT k, int bytes) {
@@ -56,22 +23,8 @@ template <> struct DrtTile<4> { static constexpr int R = 8, T = 64; };
 template <int K, class In, class Acc, class Out, bool FIRST, bool FINAL>
 drt3d_status launch_drt_k(const DrtPass &prm, int ninst, cudaStream_t st) {
     constexpr int R = DrtTile<K>::R, T = DrtTile<K>::T;
-    using G = DrtGeom<K, R, T>;
+    using G = DrtGeom<K, R, T, !FIRST && sizeof(In) == 2>;
     auto kern = drt_pass_kernel<K, R, T, In, Acc, Out, FIRST, FINAL>;
-    static bool attr_ok = set_smem(kern, G::SMEM);
-    if (!attr_ok) return DRT3D_ERR_CUDA;
-    const int ntiles = (prm.out_width + T - 1) / T;
-    const long long groups = 1LL << (2 * (prm.c + prm.m));
-    dim3 grid(ntiles, (unsigned)groups, ninst);
-    kern<<<grid, G::THREADS, G::SMEM, st>>>(prm);
-    return DRT3D_OK;
-}
-
-template <int K, class MidIn, class Acc, class Out, bool FINAL>
-drt3d_status launch_drt_mid_k(const DrtPass &prm, int ninst, cudaStream_t st) {
-    constexpr int R = DrtTile<K>::R, T = DrtTile<K>::T;
-    using G = DrtMidGeom<K, R, T, MidIn>;
-    auto kern = drt_pass_mid_kernel<K, R, T, MidIn, Acc, Out, FINAL>;
     static bool attr_ok = set_smem(kern, G::SMEM);
     if (!attr_ok) return DRT3D_ERR_CUDA;
     const int ntiles = (prm.out_width + T - 1) / T;
@@ -83,15 +36,6 @@ drt3d_status launch_drt_mid_k(const DrtPass &prm, int ninst, cudaStream_t st) {
 
 template <class In, class Acc, class Out, bool FIRST, bool FINAL>
 drt3d_status launch_drt(int K, const DrtPass &prm, int ninst, cudaStream_t st) {
-    if constexpr (!FIRST) {
-        switch (K) {
-            case 1: return launch_drt_mid_k<1, In, Acc, Out, FINAL>(prm, ninst, st);
-            case 2: return launch_drt_mid_k<2, In, Acc, Out, FINAL>(prm, ninst, st);
-            case 3: return launch_drt_mid_k<3, In, Acc, Out, FINAL>(prm, ninst, st);
-            case 4: return launch_drt_mid_k<4, In, Acc, Out, FINAL>(prm, ninst, st);
-        }
-        return DRT3D_ERR_UNSUPPORTED;
-    }
     switch (K) {
         case 1: return launch_drt_k<1, In, Acc, Out, FIRST, FINAL>(prm, ninst, st);
         case 2: return launch_drt_k<2, In, Acc, Out, FIRST, FINAL>(prm, ninst, st);
