@@ -164,11 +164,12 @@ drt3d_status make_plan(int transform, int N, uint32_t mask, const drt3d_opts &o,
         if (transform == 0) {
             if (p == P.npass) { P.base[p] = 0; P.width[p] = 3 * N; P.pitch[p] = 3 * N; }
             else {
-                // stage-c support starts at D = 2N - 2(2^c - 1) (eq:3Dfm); the stored
-                // origin is rounded down to 16 so that the next pass' tiles start 16-aligned, and
-                // rows are computed (zero-padded) up to their pitch so any 16-byte chunk inside a
-                // row is valid data.
-                P.base[p] = (2 * N - 2 * ((1 << c) - 1)) / 16 * 16;
+                // stage-c support starts at D = 2N - 2(2^c - 1) (eq:3Dfm).  Rows are
+                // stored pre-shifted left by rho < 8 elements,
+                // so the stored origin sits at least 7 below the support, rounded down to 16 so
+                // that every reader window starts on a 16-byte chunk; rows are computed
+                // (zero-padded) up to their pitch so any 16-byte chunk inside a row is valid data.
+                P.base[p] = (2 * N - 2 * ((1 << c) - 1) - 7) / 16 * 16;
                 P.pitch[p] = round_up(3 * N - P.base[p], 16);
                 P.width[p] = P.pitch[p];
             }
@@ -306,6 +307,7 @@ drt3d_status run_drt(const void *cube, uint32_t mask, void *out, const drt3d_opt
             prm.out_pitch = P.pitch[p + 1];
             prm.out_base = P.base[p + 1];
             prm.out_width = P.width[p + 1];
+            prm.next_k = fin ? 0 : P.ks[p + 1];
             drt3d_status s = DRT3D_OK;
             drt3d_status ls = L.run(first ? 0 : (fin ? 2 : 1), [&] {
                 s = dispatch_drt(o.in_dtype, P.ks[p], P.stor[p], P.stor[p + 1], first, fin, prm, ninst, st);

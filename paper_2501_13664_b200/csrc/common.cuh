@@ -58,6 +58,82 @@ template <> __device__ __forceinline__ uint16_t to_out<uint16_t, uint32_t>(uint3
 template <> __device__ __forceinline__ uint32_t to_out<uint32_t, uint32_t>(uint32_t v) { return v; }
 template <> __device__ __forceinline__ float to_out<float, float>(float v) { return v; }
 
+// ---------------------------------------------------------------------------
+// Residual pre-shift of intermediate rows.
+// A pass reads stage-c row (s, v) starting at D + s1 w1 + s2 w2 (w = v mod 2^K);
+// the writer stores that row shifted left by rho = (s1 w1 + s2 w2) mod EPC
+// (EPC = elements per 16-byte chunk), so every reader window starts on a chunk
+// boundary and staging is a plain aligned copy.  The writer realigns its
+// register runs with one warp shuffle per word and a select network.
+
+// o[i] = w[i + s] for a runtime word shift s in [0, 3] (two SEL stages).
+template <int NO, int NW>
+__device__ __forceinline__ void shift_words(const uint32_t (&w)[NW], int s, uint32_t (&o)[NO]) {
+    static_assert(NW >= NO + 3, "window");
+    uint32_t t[NO + 1];
+#pragma unroll
+    for (int i = 0; i < NO + 1; ++i) t[i] = (s & 2) ? w[i + 2] : w[i];
+#pragma unroll
+    for (int i = 0; i < NO; ++i) o[i] = (s & 1) ? t[i + 1] : t[i];
+}
+
+// 16-byte chunk = window elements [rho, rho + EPC) of a window of 32-bit words
+// holding E = 4 / sizeof(elem) elements each (E = 2: u16 pairs, E = 1: 32-bit).
+template <int E, int NW>
+__device__ __forceinline__ void window_chunk(const uint32_t (&w)[NW], int rho, int q, uint32_t (&o)[4]) {
+    // q = chunk index inside the window (the window starts at a chunk boundary)
+    if constexpr (E == 2) {
+        uint32_t t[5];
+        uint32_t ww[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) ww[i] = (4 * q + i < NW) ? w[4 * q + i] : 0u;
+        shift_words<5, 8>(ww, rho >> 1, t);
+        const uint32_t sel = (rho & 1) ? 0x5432u : 0x3210u;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) o[i] = __byte_perm(t[i], t[i + 1], sel);
+    } else {
+        uint32_t ww[7];
+#pragma unroll
+        for (int i = 0; i < 7; ++i) ww[i] = (4 * q + i < NW) ? w[4 * q + i] : 0u;
+        shift_words<4, 7>(ww, rho, o);
+    }
+}
+
+__device__ __forceinline__ uint32_t sel4(const uint32_t (&v)[4], int i) {
+    const uint32_t lo = (i & 1) ? v[1] : v[0], hi = (i & 1) ? v[3] : v[2];
+    return (i & 2) ? hi : lo;
+}
+
+// Store elements [0, m) (head) or [EPC - t, EPC) (tail) of a 16-byte chunk
+// with naturally aligned 8/4/2-byte stores.  E = elements per 32-bit word.
+// (Runtime word choices go through selects, not register-array indexing.)
+template <int E>
+__device__ __forceinline__ void store_chunk_head(void *chunk, const uint32_t (&v)[4], int m) {
+    unsigned char *p = reinterpret_cast<unsigned char *>(chunk);
+    if (m >= 4 * E) { *reinterpret_cast<uint4 *>(p) = make_uint4(v[0], v[1], v[2], v[3]); return; }
+    const int mb = m * (4 / E);                         // bytes to write, < 16
+    if (mb & 8) *reinterpret_cast<uint2 *>(p) = make_uint2(v[0], v[1]);
+    const int w4 = (mb & 8) ? 2 : 0;
+    if (mb & 4) *reinterpret_cast<uint32_t *>(p + 4 * w4) = sel4(v, w4);
+    if (E == 2 && (mb & 2)) {
+        const int w2 = w4 + ((mb & 4) ? 1 : 0);
+        *reinterpret_cast<uint16_t *>(p + 4 * w2) = (uint16_t)(sel4(v, w2) & 0xFFFFu);
+    }
+}
+template <int E>
+__device__ __forceinline__ void store_chunk_tail(void *chunk, const uint32_t (&v)[4], int t) {
+    unsigned char *p = reinterpret_cast<unsigned char *>(chunk);
+    if (t >= 4 * E) { *reinterpret_cast<uint4 *>(p) = make_uint4(v[0], v[1], v[2], v[3]); return; }
+    const int tb = t * (4 / E);                         // bytes to write at the end, < 16
+    int b = 16 - tb;                                    // first byte written
+    if (E == 2 && (tb & 2)) {                           // odd u16 count: one u16 at an odd index
+        *reinterpret_cast<uint16_t *>(p + b) = (uint16_t)(sel4(v, b >> 2) >> 16);
+        b += 2;
+    }
+    if (tb & 4) { *reinterpret_cast<uint32_t *>(p + b) = sel4(v, b >> 2); b += 4; }
+    if (tb & 8) *reinterpret_cast<uint2 *>(p + 8) = make_uint2(v[2], v[3]);
+}
+
 // streaming (evict-first) 16-byte global store for final outputs that are
 // never re-read by this call.
 __device__ __forceinline__ void st_cs_v4(void *p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {

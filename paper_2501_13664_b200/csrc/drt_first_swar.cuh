@@ -1,0 +1,273 @@
+// drt_first_swar.cuh -- first DRT pass for u8 voxels with two 16-bit lanes per
+// 32-bit register (SWAR; the paper's "narrow integer" idea).
+//
+// The first pass (stages 0..K-1, K <= 4) of a u8 cube produces stage-K sums of
+// at most 255 * 4^K <= 65280 voxels' worth, and its x-step sums (16 voxels)
+// at most 4080: both fit a 16-bit lane, and a 32-bit add of two packed words
+// never carries between lanes.  With the pass identity of drt_kernels.cuh
+//
+//   X(r1, w2)[e]  = sum_{w1} f(w1, w2)[e + l^K_{r1}(w1)]           (x-step)
+//   out(r1, r2)[e] = sum_{w2} X(r1, w2)[e + l^K_{r2}(w2)]          (y-step)
+//
+// the x-step offsets do not depend on w2 and the y-step offsets do not depend
+// on r1.  So the x-step runs on rows packed as (w2, w2 + S/2) and the y-step
+// on X rows packed as (r1, r1 + S/2); one lane swap between the steps turns
+// the first packing into the second.  Each add instruction thus serves two
+// outputs, at the same tile shape as the 32-bit kernel.
+#pragma once
+#include "drt_kernels.cuh"
+
+namespace d3 {
+
+template <int K, int R, int T>
+struct SwarGeom {
+    static constexpr int S = 1 << K;
+    static constexpr int H2 = S / 2;                      // lane pairing distance
+    static constexpr int H = S - 1;
+    static constexpr int WIN = T + 2 * H;
+    static constexpr int NRX = (T + H + R - 1) / R;
+    static constexpr int NRY = T / R;
+    static constexpr int RD = (NRX - 1) * R + (R + H + 3) / 4 * 4;
+    static constexpr int BW = ((WIN > RD ? WIN : RD) + 15) / 16 * 16;   // staged words per slot
+    static constexpr int XB = NRX * R * 4;
+    static constexpr int SP0 = (BW * 4 > XB ? BW * 4 : XB);
+    static constexpr int SP = SP0 + 16;                   // slot pitch (bytes); +16 rotates banks
+    static constexpr int NSLOT = S * H2;                  // packed slots
+    static constexpr int XT = H2 * NRX;                   // x-step tasks
+    static constexpr int YT = H2 * NRY;                   // y-step tasks
+    static constexpr int THREADS = ((XT > YT ? XT : YT) + 31) / 32 * 32;
+    static constexpr int ORW = T / 2;                     // output staging: words per row (power of 2)
+    static constexpr int ORP = ORW * 4 + 16;              // output staging row pitch (bytes)
+    static constexpr int SMEM0 = NSLOT * SP;
+    static constexpr int SMEM = (SMEM0 > S * S * ORP ? SMEM0 : S * S * ORP);
+    static constexpr int CTAS = 4;                        // target CTAs per SM
+    static constexpr int MAXREG0 = 65536 / (CTAS * THREADS) / 8 * 8;
+    static constexpr int MAXREG = MAXREG0 > 255 ? 255 : MAXREG0;
+    static_assert(T % R == 0 && R == 8, "tile shape");
+    static_assert(NRY == 8 || NRY == 16, "y runs per row must be a shuffle width");
+};
+
+// word = lo | hi << 16 for the four byte pairs (a.b_i, b.b_i): 6 PRMT per 4 words
+__device__ __forceinline__ void pair_bytes(uint32_t a, uint32_t b, uint32_t (&w)[4]) {
+    const uint32_t t0 = __byte_perm(a, b, 0x5140), t1 = __byte_perm(a, b, 0x7362);
+    w[0] = __byte_perm(t0, 0u, 0x4140);
+    w[1] = __byte_perm(t0, 0u, 0x4342);
+    w[2] = __byte_perm(t1, 0u, 0x4140);
+    w[3] = __byte_perm(t1, 0u, 0x4342);
+}
+__device__ __forceinline__ uint4 rev16(uint4 v) {
+    return make_uint4(__byte_perm(v.w, 0, 0x0123), __byte_perm(v.z, 0, 0x0123), __byte_perm(v.y, 0, 0x0123),
+                      __byte_perm(v.x, 0, 0x0123));
+}
+
+template <int K, int R, int T>
+__global__ void __launch_bounds__(SwarGeom<K, R, T>::THREADS) __maxnreg__((SwarGeom<K, R, T>::MAXREG))
+drt_first_swar_kernel(const DrtPass p) {
+    using G = SwarGeom<K, R, T>;
+    constexpr int S = G::S, H2 = G::H2, SP = G::SP, BW = G::BW;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    unsigned char *sm = smem_raw;
+
+    const int tid = threadIdx.x;
+    const int tile = blockIdx.x, g = blockIdx.y, li = blockIdx.z;
+    const int inst = p.inst0 + li;
+    const int m = p.m;                                    // c = 0: the group is (V1, V2) only
+    const int V2 = g & ((1 << m) - 1);
+    const int V1 = (g >> m) & ((1 << m) - 1);
+    const int d0 = tile * T;
+    const int Dabs = p.out_base + d0;
+    const int N = p.N;
+
+    auto put4 = [&](int slot, int chunk, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+        *reinterpret_cast<uint4 *>(sm + slot * SP + 16 * xswz(chunk)) = make_uint4(a, b, c, d);
+    };
+
+    // ---- stage packed rows: slot (w1, pw), word e = f(w1, pw)[e] | f(w1, pw + H2)[e] << 16,
+    // f(w1, w2)[e] = oriented voxel (xb + w1, yb + w2, z0 + e), 0 outside the cube.
+    {
+        const Orient o = p.ori[inst % p.ndod];
+        const uint8_t *cube = reinterpret_cast<const uint8_t *>(p.in) + (long long)(inst / p.ndod) * N * N * N;
+        const int z0 = Dabs - 2 * N;                      // stage 0: D = z' + 2N
+        const int xb = V1 << K, yb = V2 << K;
+        auto vox = [&](int x, int y, int z) -> const uint8_t * {
+            return cube + o.off0 + (long long)x * o.sx + (long long)y * o.sy + (long long)z * o.sz;
+        };
+        if (K == 4 && p.vec_ok && o.fast == 2 && (z0 & 15) == 0) {
+            // z' contiguous (forward): two LDG.128 (rows pw, pw + 8) -> 16 packed words
+            constexpr int NQ = BW / 16;
+            for (int it = tid; it < G::NSLOT * NQ; it += blockDim.x) {
+                const int slot = it / NQ, q = it - slot * NQ;
+                const int w1 = slot / H2, pw = slot - w1 * H2, z = z0 + 16 * q;
+                uint4 a = make_uint4(0u, 0u, 0u, 0u), b = a;
+                if ((unsigned)z < (unsigned)N) {
+                    a = __ldg(reinterpret_cast<const uint4 *>(vox(xb + w1, yb + pw, z)));
+                    b = __ldg(reinterpret_cast<const uint4 *>(vox(xb + w1, yb + pw + H2, z)));
+                }
+                const uint32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    uint32_t w[4];
+                    pair_bytes(av[h], bv[h], w);
+                    put4(slot, 4 * q + h, w[0], w[1], w[2], w[3]);
+                }
+            }
+        } else if (K == 4 && p.vec_ok && o.fast == 1) {
+            // y' contiguous: one LDG.128 along y' = all 16 w2 of (w1, z'); 4 consecutive z' per item
+            const bool fwd = o.sy > 0;
+            constexpr int NE4 = BW / 4;
+            for (int it = tid; it < S * NE4; it += blockDim.x) {
+                const int w1 = it / NE4, e4 = it - w1 * NE4;
+                uint32_t wd[4][H2];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const int z = z0 + 4 * e4 + t;
+                    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+                    if ((unsigned)z < (unsigned)N)
+                        v = __ldg(reinterpret_cast<const uint4 *>(vox(xb + w1, yb + (fwd ? 0 : 15), z)));
+                    if (!fwd) v = rev16(v);                // byte b <-> w2 = b
+                    uint32_t lo[4], hi[4];
+                    pair_bytes(v.x, v.z, lo);              // w2 = 0..3 with 8..11
+                    pair_bytes(v.y, v.w, hi);              // w2 = 4..7 with 12..15
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        wd[t][j] = lo[j];
+                        wd[t][4 + j] = hi[j];
+                    }
+                }
+#pragma unroll
+                for (int pw = 0; pw < H2; ++pw) put4(w1 * H2 + pw, e4, wd[0][pw], wd[1][pw], wd[2][pw], wd[3][pw]);
+            }
+        } else if (K == 4 && p.vec_ok && o.fast == 0) {
+            // x' contiguous: LDG.128 along x' = all 16 w1 of (w2, z'); rows pw and pw + 8
+            const bool fwd = o.sx > 0;
+            constexpr int NE4 = BW / 4;
+            for (int it = tid; it < H2 * NE4; it += blockDim.x) {
+                const int pw = it / NE4, e4 = it - pw * NE4;
+                uint32_t wd[4][S];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const int z = z0 + 4 * e4 + t;
+                    uint4 a = make_uint4(0u, 0u, 0u, 0u), b = a;
+                    if ((unsigned)z < (unsigned)N) {
+                        a = __ldg(reinterpret_cast<const uint4 *>(vox(xb + (fwd ? 0 : 15), yb + pw, z)));
+                        b = __ldg(reinterpret_cast<const uint4 *>(vox(xb + (fwd ? 0 : 15), yb + pw + H2, z)));
+                    }
+                    if (!fwd) {
+                        a = rev16(a);
+                        b = rev16(b);
+                    }
+                    const uint32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        uint32_t w[4];
+                        pair_bytes(av[h], bv[h], w);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) wd[t][4 * h + j] = w[j];
+                    }
+                }
+#pragma unroll
+                for (int w1 = 0; w1 < S; ++w1) put4(w1 * H2 + pw, e4, wd[0][w1], wd[1][w1], wd[2][w1], wd[3][w1]);
+            }
+        } else {
+            // generic (small N, any orientation): word by word
+            for (int it = tid; it < G::NSLOT * BW; it += blockDim.x) {
+                const int slot = it / BW, e = it - slot * BW;
+                const int w1 = slot / H2, pw = slot - w1 * H2, z = z0 + e;
+                uint32_t bits = 0;
+                if ((unsigned)z < (unsigned)N)
+                    bits = (uint32_t)__ldg(vox(xb + w1, yb + pw, z)) | ((uint32_t)__ldg(vox(xb + w1, yb + pw + H2, z)) << 16);
+                *reinterpret_cast<uint32_t *>(sm + slot * SP + 16 * xswz(e >> 2) + 4 * (e & 3)) = bits;
+            }
+        }
+    }
+    __syncthreads();
+
+    // ---- x-step on (w2, w2 + H2) pairs, then y-step on (r1, r1 + H2) pairs; one code path.
+    //   step 0: thread (pw, run)  -> acc[r1][j] = (X(r1, pw), X(r1, pw + H2))
+    //   step 1: thread (q, run)   -> acc[r2][j] = (out(q, r2), out(q + H2, r2))
+    uint32_t acc[S][R];
+#pragma unroll 1
+    for (int step = 0; step < 2; ++step) {
+        const int nr = step ? G::NRY : G::NRX;
+        const int grp = tid / nr, run = tid - grp * nr;
+        const bool act = tid < (step ? G::YT : G::XT);
+        if (act) {
+#pragma unroll
+            for (int i = 0; i < S; ++i)
+#pragma unroll
+                for (int j = 0; j < R; ++j) acc[i][j] = 0u;
+            drt_accumulate<K, R, SP, false, uint32_t, false>(sm, step ? grp * S : grp, step ? 1 : H2, run * (R / 4),
+                                                             p.one, acc);
+        }
+        __syncthreads();
+        if (act) {
+            if (step == 0) {
+                // lane swap: X slot (q, w2) = (X(q, w2), X(q + H2, w2)), written in place
+#pragma unroll
+                for (int q = 0; q < H2; ++q) {
+#pragma unroll
+                    for (int c = 0; c < R / 4; ++c) {
+                        uint32_t lo[4], hi[4];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            lo[j] = __byte_perm(acc[q][4 * c + j], acc[q + H2][4 * c + j], 0x5410);
+                            hi[j] = __byte_perm(acc[q][4 * c + j], acc[q + H2][4 * c + j], 0x7632);
+                        }
+                        put4(q * S + grp, run * (R / 4) + c, lo[0], lo[1], lo[2], lo[3]);
+                        put4(q * S + grp + H2, run * (R / 4) + c, hi[0], hi[1], hi[2], hi[3]);
+                    }
+                }
+            } else {
+                // unpack to u16 output rows in SMEM: row (r1, r2) at ORP * (r1 * S + r2)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t sel = h ? 0x7632u : 0x5410u;
+#pragma unroll
+                    for (int r2 = 0; r2 < S; ++r2) {
+                        uint32_t w[R / 2];
+#pragma unroll
+                        for (int i = 0; i < R / 2; ++i) w[i] = __byte_perm(acc[r2][2 * i], acc[r2][2 * i + 1], sel);
+                        *reinterpret_cast<uint4 *>(sm + G::ORP * ((grp + h * H2) * S + r2) + 2 * R * run) =
+                            make_uint4(w[0], w[1], w[2], w[3]);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---- copy-out: stage-K rows stored pre-shifted by rho (common.cuh).  Item (row, k): k = 0 is
+    // the tail of the chunk before the tile (tile elements [0, rho)), k >= 1 the chunk holding tile
+    // elements [8(k-1) + rho, 8k + rho) (a head store when it runs past the tile).
+    uint16_t *outp = reinterpret_cast<uint16_t *>(p.out);
+    const long long out_inst = (long long)li * p.out_inst_stride;
+    const int mK = (1 << p.next_k) - 1;
+    const int wv1 = V1 & mK, wv2 = V2 & mK;
+    constexpr int NK = T / 8 + 1;
+    for (int it = tid; it < S * S * NK; it += blockDim.x) {
+        const int rr = it / NK, k = it - rr * NK;
+        const int r1 = rr / S, r2 = rr - r1 * S;
+        const int rho = (r1 * wv1 + r2 * wv2) & 7;
+        const int s0 = 8 * (k - 1) + rho;                 // first tile element of the chunk (k >= 1)
+        const int pc = d0 + 8 * (k - 1);                  // stored element index of the chunk
+        if (k == 0 ? (rho == 0 || d0 < 8) : (pc >= p.out_width)) continue;
+        const long long row = ((((long long)r1 << K) + r2) << (2 * m)) + ((long long)V1 << m) + V2;
+        uint16_t *dst = outp + out_inst + row * p.out_pitch + pc;
+        const uint32_t *srow = reinterpret_cast<const uint32_t *>(sm + G::ORP * rr);
+        const int sw = (k == 0 ? rho - 8 : s0);           // tile element at chunk position 0
+        // words covering tile elements [sw, sw + 8); indices below 0 only feed masked positions
+        const int w0 = sw >> 1;
+        uint32_t w[5];
+#pragma unroll
+        for (int i = 0; i < 5; ++i) w[i] = srow[(w0 + i) & (G::ORW - 1)];
+        const uint32_t sel = (sw & 1) ? 0x5432u : 0x3210u;
+        uint32_t v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[i] = __byte_perm(w[i], w[i + 1], sel);
+        if (k == 0) store_chunk_tail<2>(dst, v, rho);
+        else if (s0 + 8 > T) store_chunk_head<2>(dst, v, T - s0);
+        else *reinterpret_cast<uint4 *>(dst) = make_uint4(v[0], v[1], v[2], v[3]);
+    }
+}
+
+}  // namespace d3

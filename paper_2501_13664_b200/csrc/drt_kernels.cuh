@@ -39,6 +39,7 @@ struct DrtPass {
     int ndod;                       // dodecants per cube (instances per batch entry)
     int layout;                     // final pass: 0 stacked, 1 mosaic
     int vec_ok;                     // first pass: 16-byte chunked cube loads are aligned (N >= 16)
+    int next_k;                     // non-final passes: radix bits of the pass that reads this output
     uint32_t one;                   // = 1; a runtime multiplier so some adds issue as IMAD (FMA pipe)
     Orient ori[kMaxDod];            // first pass: per-dodecant-slot orientation
     int8_t out_order[kMaxDod][2];   // mosaic: OutOrder[k][0..1]
@@ -55,13 +56,11 @@ struct DrtGeom {
     static constexpr int EPS = STAGE16 ? 8 : 4;           // staged elements per 16-byte chunk
     static constexpr int RD = (NRX - 1) * R + (R + H + EPS - 1) / EPS * EPS;   // staged elements the x-step touches
     static constexpr int BW = ((WIN > RD ? WIN : RD) + 15) / 16 * 16; // staged elements per row
-    // slot layout (bytes): STAGE16 (u16 stage-c rows): [staged u16 | raw aligned source chunks],
-    // otherwise [staged 32-bit]; X (32-bit, NRX*R words, XOR-swizzled chunks) is written in place.
+    // slot layout (bytes): staged row (u16 when STAGE16, else 32-bit with XOR-swizzled chunks);
+    // X (32-bit, NRX*R words, XOR-swizzled chunks) is written in place over it.
     static constexpr int STAGED = BW * (STAGE16 ? 2 : 4);
-    static constexpr int RAWOFF = STAGED;
-    static constexpr int NRAW = STAGE16 ? BW / 8 + 1 : 0; // raw 16-byte chunks per slot
     static constexpr int XB = NRX * R * 4;
-    static constexpr int SP0 = (STAGED + 16 * NRAW > XB ? STAGED + 16 * NRAW : XB);
+    static constexpr int SP0 = (STAGED > XB ? STAGED : XB);
     static constexpr int SP = (SP0 + 15) / 16 * 16 + 16;  // slot pitch; +16 rotates banks per slot
     static constexpr int XT = S * NRX;                    // x-step tasks
     static constexpr int YT = S * NRY;                    // y-step tasks
@@ -96,7 +95,7 @@ __device__ __forceinline__ Acc add2(Acc acc, uint32_t x, uint32_t y, uint32_t on
     }
 }
 
-template <int K, int R, int SP, bool U16, class Acc>
+template <int K, int R, int SP, bool U16, class Acc, bool FMA_SPLIT = true>
 __device__ __forceinline__ void drt_accumulate(const unsigned char *__restrict__ sm, int slot0, int sstep, int c0,
                                                uint32_t one, Acc (&acc)[1 << K][R]) {
     constexpr int S = 1 << K;
@@ -138,7 +137,7 @@ __device__ __forceinline__ void drt_accumulate(const unsigned char *__restrict__
             static_for<0, S>([&](auto r_) {
                 constexpr int r = decltype(r_)::value;
                 constexpr int o0 = lk(K, r, a0), o1 = lk(K, r, a1);
-                constexpr bool fma = (r % 8) < 3;
+                constexpr bool fma = FMA_SPLIT && (r % 8) < 3;
 #pragma unroll
                 for (int j = 0; j < R; ++j) acc[r][j] = add2<Acc>(acc[r][j], b0[j + o0], b1[j + o1], one, fma);
             });
@@ -152,19 +151,6 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool va
 }
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
-}
-
-// NW output words starting `b` bytes (0..15) into the window w[0 .. NW + 3].
-template <int NW>
-__device__ __forceinline__ void realign_words(const uint32_t *w, int b, uint32_t *o) {
-    const int ws = b >> 2, bs = (b & 3) * 8;
-    uint32_t t[NW + 2], u[NW + 1];
-#pragma unroll
-    for (int i = 0; i < NW + 2; ++i) t[i] = (ws & 2) ? w[i + 2] : w[i];
-#pragma unroll
-    for (int i = 0; i < NW + 1; ++i) u[i] = (ws & 1) ? t[i + 1] : t[i];
-#pragma unroll
-    for (int i = 0; i < NW; ++i) o[i] = __funnelshift_r(u[i], u[i + 1], bs);
 }
 
 template <int K, int R, int T, class In, class Acc, class Out, bool FIRST, bool FINAL>
@@ -214,9 +200,10 @@ drt_pass_kernel(const DrtPass p) {
     };
     const bool mosaic = FINAL && p.layout == 1;
 
-    // ---- tiles entirely outside the support of all 4^K output rows: zeros
-    // (support D >= 2N - s1 - s2)
-    {
+    // ---- final tiles entirely outside the support of all 4^K output rows: zeros
+    // (support D >= 2N - s1 - s2).  Intermediate tiles are always computed so
+    // that their pre-shifted chunks are written by exactly one pattern.
+    if constexpr (FINAL) {
         const int s1max = (sg1 << K) + S - 1, s2max = (sg2 << K) + S - 1;
         if (Dabs + T <= 2 * N - s1max - s2max) {
             constexpr int EPV = 16 / (int)sizeof(Out);
@@ -330,128 +317,32 @@ drt_pass_kernel(const DrtPass p) {
                 put(slot, e, bits);
             }
         }
-    } else if constexpr (STAGE16) {
-        // u16 stage-c rows.  Phase 1: cp.async the NRAW aligned 16-byte source chunks that cover
-        // the slot's range [st, st + BW) (st = tile origin + pre-shift s1 w1 + s2 w2) into the
-        // slot's raw area -- asynchronous, no registers, out-of-row chunks zero-filled.  Phase 2:
-        // realign each slot by its runtime byte offset into the staged u16 row.
-        const In *inb = reinterpret_cast<const In *>(p.in) + (long long)li * p.in_inst_stride;
-        const int nc = p.n - c;
-        const long long rbase = (((long long)sg1 << c) + sg2) << (2 * nc);
-        const int nchunk = p.in_width >> 3;                 // chunks per stored row (width = pitch)
-        constexpr int NRAW = G::NRAW, HALF = (NRAW + 1) / 2;
-        for (int it = tid; it < S * S * 2; it += blockDim.x) {
-            const int slot = it >> 1, h = it & 1;
-            const int w1 = slot >> K, w2 = slot & (S - 1);
-            const long long row = rbase + ((long long)((V1 << K) + w1) << nc) + (V2 << K) + w2;
-            const int st = Dabs + sg1 * w1 + sg2 * w2 - p.in_base;
-            const int c0 = st >> 3;
-            const uint4 *src = reinterpret_cast<const uint4 *>(inb + row * p.in_pitch);
-            unsigned char *raw = sm + slot * SP + G::RAWOFF;
-#pragma unroll
-            for (int k = 0; k < HALF; ++k) {
-                const int kk = h * HALF + k;
-                if (kk < NRAW) {
-                    const int cc = c0 + kk;
-                    const bool ok = (unsigned)cc < (unsigned)nchunk;
-                    cp_async16(raw + 16 * kk, ok ? (const void *)(src + cc) : (const void *)inb, ok);
-                }
-            }
-        }
-        cp_async_wait_all();
-        __syncthreads();
-        constexpr int NQS = BW / 8;
-        constexpr int PQ = NQS % 6 == 0 ? 6 : (NQS % 4 == 0 ? 4 : (NQS % 3 == 0 ? 3 : 2));
-        constexpr int NPART = NQS / PQ;
-        static_assert(NQS % PQ == 0, "staging split");
-        for (int it = tid; it < S * S * NPART; it += blockDim.x) {
-            const int slot = it / NPART, part = it - slot * NPART;
-            const int w1 = slot >> K, w2 = slot & (S - 1);
-            const int bsh = ((Dabs + sg1 * w1 + sg2 * w2 - p.in_base) & 7) * 2;
-            const unsigned char *raw = sm + slot * SP + G::RAWOFF + 16 * part * PQ;
-            uint32_t w[4 * (PQ + 1)];
-#pragma unroll
-            for (int k = 0; k <= PQ; ++k) {
-                const uint4 v = *reinterpret_cast<const uint4 *>(raw + 16 * k);
-                w[4 * k + 0] = v.x;
-                w[4 * k + 1] = v.y;
-                w[4 * k + 2] = v.z;
-                w[4 * k + 3] = v.w;
-            }
-            uint32_t o[4 * PQ];
-            realign_words<4 * PQ>(w, bsh, o);
-#pragma unroll
-            for (int k = 0; k < PQ; ++k)
-                *reinterpret_cast<uint4 *>(sm + slot * SP + 16 * (part * PQ + k)) =
-                    make_uint4(o[4 * k], o[4 * k + 1], o[4 * k + 2], o[4 * k + 3]);
-        }
     } else {
-        // stage-c rows: the slot's staged element e is stored element st + e of its row, st =
-        // tile origin + pre-shift s1 w1 + s2 w2.  Aligned 16-byte loads of PQ+1 consecutive chunks
-        // are realigned in registers to the row's runtime byte offset, then widened to 32 bits.
-        constexpr int EPC = 16 / (int)sizeof(In);         // source elements per 16-byte chunk
+        // stage-c rows, stored with the residual pre-shift (writer side, DESIGN.md "Aligned stage
+        // buffers"): the slot's window starts at stored element
+        //   (Dabs - in_base) + EPC * floor((s1 w1 + s2 w2) / EPC),
+        // a chunk boundary, so staging is a plain aligned 16-byte copy (cp.async, zero-filled
+        // outside the stored row).  Consecutive threads take consecutive chunks of one row.
+        constexpr int EPC = 16 / (int)sizeof(In);          // stored elements per 16-byte chunk
         constexpr int LOG_EPC = EPC == 8 ? 3 : 2;
-        constexpr int NQS = BW / EPC;                      // source chunks per slot
-        constexpr int PQ = NQS % 6 == 0 ? 6 : (NQS % 4 == 0 ? 4 : (NQS % 3 == 0 ? 3 : 2));
-        constexpr int NPART = NQS / PQ;
-        static_assert(NQS % PQ == 0, "staging split");
+        constexpr int NCH = BW / EPC;                      // chunks per staged row
+        static_assert(BW % EPC == 0, "staging chunks");
         const In *inb = reinterpret_cast<const In *>(p.in) + (long long)li * p.in_inst_stride;
         const int nc = p.n - c;
         const long long rbase = (((long long)sg1 << c) + sg2) << (2 * nc);
         const int nchunk = p.in_width >> LOG_EPC;          // chunks per stored row (width = pitch)
-        constexpr int ITEMS = 2;                           // items whose loads are in flight together
-        for (int base = tid; base < S * S * NPART; base += blockDim.x * ITEMS) {
-            uint32_t w[ITEMS][4 * (PQ + 1)];
-            int bsh[ITEMS], slot_[ITEMS], part_[ITEMS];
-#pragma unroll
-            for (int u = 0; u < ITEMS; ++u) {
-                const int it = base + u * blockDim.x;
-                slot_[u] = -1;
-                bsh[u] = 0;
-                int c0 = -1 << 20;
-                const uint4 *src = nullptr;
-                if (it < S * S * NPART) {
-                    const int slot = it / NPART, part = it - slot * NPART;
-                    const int w1 = slot >> K, w2 = slot & (S - 1);
-                    const long long row = rbase + ((long long)((V1 << K) + w1) << nc) + (V2 << K) + w2;
-                    const int st = Dabs + sg1 * w1 + sg2 * w2 - p.in_base;
-                    c0 = (st >> LOG_EPC) + part * PQ;          // arithmetic shift = floor division
-                    bsh[u] = (st & (EPC - 1)) * (int)sizeof(In);
-                    slot_[u] = slot;
-                    part_[u] = part;
-                    src = reinterpret_cast<const uint4 *>(inb + row * p.in_pitch);
-                }
-#pragma unroll
-                for (int k = 0; k <= PQ; ++k) {
-                    uint4 v = make_uint4(0u, 0u, 0u, 0u);
-                    if ((unsigned)(c0 + k) < (unsigned)nchunk) v = __ldg(src + c0 + k);
-                    w[u][4 * k + 0] = v.x;
-                    w[u][4 * k + 1] = v.y;
-                    w[u][4 * k + 2] = v.z;
-                    w[u][4 * k + 3] = v.w;
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < ITEMS; ++u) {
-                if (slot_[u] < 0) continue;
-                const int slot = slot_[u], part = part_[u];
-                uint32_t o[4 * PQ];
-                realign_words<4 * PQ>(w[u], bsh[u], o);
-                if constexpr (sizeof(In) == 2) {
-#pragma unroll
-                    for (int k = 0; k < PQ; ++k) {
-                        const int ch = 2 * (part * PQ + k);     // two 32-bit chunks per source chunk
-                        put4(slot, ch, make_uint4(o[4 * k] & 0xFFFFu, o[4 * k] >> 16, o[4 * k + 1] & 0xFFFFu, o[4 * k + 1] >> 16));
-                        put4(slot, ch + 1,
-                             make_uint4(o[4 * k + 2] & 0xFFFFu, o[4 * k + 2] >> 16, o[4 * k + 3] & 0xFFFFu, o[4 * k + 3] >> 16));
-                    }
-                } else {
-#pragma unroll
-                    for (int k = 0; k < PQ; ++k)
-                        put4(slot, part * PQ + k, make_uint4(o[4 * k], o[4 * k + 1], o[4 * k + 2], o[4 * k + 3]));
-                }
-            }
+        const int cb = (Dabs - p.in_base) >> LOG_EPC;      // exact: Dabs - in_base is a multiple of 16
+        for (int it = tid; it < S * S * NCH; it += blockDim.x) {
+            const int slot = it / NCH, q = it - slot * NCH;
+            const int w1 = slot >> K, w2 = slot & (S - 1);
+            const long long row = rbase + ((long long)((V1 << K) + w1) << nc) + (V2 << K) + w2;
+            const int cc = cb + ((sg1 * w1 + sg2 * w2) >> LOG_EPC) + q;
+            const bool ok = (unsigned)cc < (unsigned)nchunk;
+            const uint4 *src = reinterpret_cast<const uint4 *>(inb + row * p.in_pitch) + cc;
+            unsigned char *dst = sm + slot * SP + 16 * (STAGE16 ? q : xswz(q));
+            cp_async16(dst, ok ? (const void *)src : (const void *)inb, ok);
         }
+        cp_async_wait_all();
     }
     __syncthreads();
 
@@ -505,6 +396,56 @@ drt_pass_kernel(const DrtPass p) {
                 __syncthreads();
             }
         }
+    }
+
+    // ---- intermediate output: rows stored pre-shifted by rho (see common.cuh), realigned
+    // across the NRY runs of a row with one shuffle per word
+    if constexpr (!FINAL) {
+        if (tid < G::YT) {
+            constexpr int E = 4 / (int)sizeof(Out);        // elements per 32-bit word
+            constexpr int EPC = 4 * E;                     // elements per 16-byte chunk
+            constexpr int NWO = R / E;                     // words per run
+            constexpr int NCK = R / EPC;                   // chunks per run
+            const int mK = (1 << p.next_k) - 1;
+            const int r1 = yb, e0 = yr * R;
+            const long long s1 = ((long long)sg1 << K) + r1;
+            const long long wv1 = V1 & mK, wv2 = V2 & mK;
+            Out *rowp = row_ptr(r1) + e0;
+#pragma unroll
+            for (int r2 = 0; r2 < S; ++r2, rowp += r2_stride) {
+                const long long s2 = ((long long)sg2 << K) + r2;
+                const int rho = (int)((s1 * wv1 + s2 * wv2) & (EPC - 1));
+                uint32_t win[NWO + 4];
+#pragma unroll
+                for (int i = 0; i < NWO; ++i) {
+                    if constexpr (E == 2) win[i] = __byte_perm(Lane<Acc>::bits(acc[r2][2 * i]), Lane<Acc>::bits(acc[r2][2 * i + 1]), 0x5410);
+                    else win[i] = Lane<Acc>::bits(acc[r2][i]);
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i) win[NWO + i] = __shfl_down_sync(0xffffffffu, win[i], 1, G::NRY);
+#pragma unroll
+                for (int q = 0; q < NCK; ++q) {
+                    uint32_t v[4];
+                    window_chunk<E>(win, rho, q, v);
+                    if (d0 + e0 + q * EPC < p.out_width) {
+                        if (yr == G::NRY - 1 && q == NCK - 1) store_chunk_head<E>(rowp + q * EPC, v, EPC - rho);
+                        else *reinterpret_cast<uint4 *>(rowp + q * EPC) = make_uint4(v[0], v[1], v[2], v[3]);
+                    }
+                }
+                if (yr == 0 && rho > 0 && d0 >= EPC) {
+                    // own elements [0, rho) end the previous chunk (whose head the previous tile wrote)
+                    uint32_t tw[NWO + 4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) tw[i] = win[i];
+#pragma unroll
+                    for (int i = 0; i < NWO; ++i) tw[4 + i] = win[i];
+                    uint32_t v[4];
+                    window_chunk<E>(tw, rho, 0, v);
+                    store_chunk_tail<E>(rowp - EPC, v, rho);
+                }
+            }
+        }
+        return;
     }
 
     // ---- store out(r1 = yb, r2, run yr)

@@ -2,6 +2,7 @@
 // the per-dtype translation units k_*.cu.
 #pragma once
 #include "dispatch.h"
+#include "drt_first_swar.cuh"
 
 namespace d3 {
 
@@ -23,11 +24,23 @@ template <> struct DrtTile<4> { static constexpr int R = 8, T = 64; };
 template <int K, class In, class Acc, class Out, bool FIRST, bool FINAL>
 drt3d_status launch_drt_k(const DrtPass &prm, int ninst, cudaStream_t st) {
     constexpr int R = DrtTile<K>::R, T = DrtTile<K>::T;
+    if constexpr (FIRST && !FINAL && K >= 3 && std::is_same<In, uint8_t>::value && std::is_same<Out, uint16_t>::value) {
+        // u8 voxels -> u16 stage-K rows: packed 16-bit lanes (drt_first_swar.cuh)
+        using SG = SwarGeom<K, R, T>;
+        auto kern = drt_first_swar_kernel<K, R, T>;
+        static bool attr_ok = set_smem(kern, SG::SMEM);
+        if (!attr_ok) return DRT3D_ERR_CUDA;
+        const int ntiles = (prm.out_width + 8 + T - 1) / T;
+        dim3 grid(ntiles, (unsigned)(1LL << (2 * prm.m)), ninst);
+        kern<<<grid, SG::THREADS, SG::SMEM, st>>>(prm);
+        return DRT3D_OK;
+    }
     using G = DrtGeom<K, R, T, !FIRST && sizeof(In) == 2>;
     auto kern = drt_pass_kernel<K, R, T, In, Acc, Out, FIRST, FINAL>;
     static bool attr_ok = set_smem(kern, G::SMEM);
     if (!attr_ok) return DRT3D_ERR_CUDA;
-    const int ntiles = (prm.out_width + T - 1) / T;
+    // intermediate outputs are stored pre-shifted by up to one chunk: cover one extra chunk
+    const int ntiles = (prm.out_width + (FINAL ? 0 : 16 / (int)sizeof(Out)) + T - 1) / T;
     const long long groups = 1LL << (2 * (prm.c + prm.m));
     dim3 grid(ntiles, (unsigned)groups, ninst);
     kern<<<grid, G::THREADS, G::SMEM, st>>>(prm);
