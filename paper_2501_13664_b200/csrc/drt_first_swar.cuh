@@ -36,8 +36,8 @@ struct SwarGeom {
     static constexpr int XT = H2 * NRX;                   // x-step tasks
     static constexpr int YT = H2 * NRY;                   // y-step tasks
     static constexpr int THREADS = ((XT > YT ? XT : YT) + 31) / 32 * 32;
-    static constexpr int ORW = T / 2;                     // output staging: words per row (power of 2)
-    static constexpr int ORP = ORW * 4 + 16;              // output staging row pitch (bytes)
+    static constexpr int ORW = T / 2;                     // output staging: words per row
+    static constexpr int ORP = (ORW + 1) * 4;             // odd word pitch: rows hit distinct banks
     static constexpr int SMEM0 = NSLOT * SP;
     static constexpr int SMEM = (SMEM0 > S * S * ORP ? SMEM0 : S * S * ORP);
     static constexpr int CTAS = 4;                        // target CTAs per SM
@@ -93,53 +93,86 @@ drt_first_swar_kernel(const DrtPass p) {
             return cube + o.off0 + (long long)x * o.sx + (long long)y * o.sy + (long long)z * o.sz;
         };
         if (K == 4 && p.vec_ok && o.fast == 2 && (z0 & 15) == 0) {
-            // z' contiguous (forward): two LDG.128 (rows pw, pw + 8) -> 16 packed words
-            constexpr int NQ = BW / 16;
-            for (int it = tid; it < G::NSLOT * NQ; it += blockDim.x) {
-                const int slot = it / NQ, q = it - slot * NQ;
-                const int w1 = slot / H2, pw = slot - w1 * H2, z = z0 + 16 * q;
-                uint4 a = make_uint4(0u, 0u, 0u, 0u), b = a;
-                if ((unsigned)z < (unsigned)N) {
-                    a = __ldg(reinterpret_cast<const uint4 *>(vox(xb + w1, yb + pw, z)));
-                    b = __ldg(reinterpret_cast<const uint4 *>(vox(xb + w1, yb + pw + H2, z)));
-                }
-                const uint32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+            // z' contiguous (forward): two LDG.128 (rows pw, pw + 8) -> 16 packed words.  Item
+            // it = slot + NSLOT * q (consecutive lanes: consecutive slots, conflict-free STS); all of
+            // a thread's loads are issued before any is consumed so their L2 latencies overlap.
+            constexpr int NQ = BW / 16, NIT = (G::NSLOT * NQ + G::THREADS - 1) / G::THREADS;
+            static_assert((G::NSLOT & (G::NSLOT - 1)) == 0, "slot count");
+            const uint8_t *vb = vox(xb, yb, z0);
+            uint4 a[NIT], b[NIT];
 #pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                    uint32_t w[4];
-                    pair_bytes(av[h], bv[h], w);
-                    put4(slot, 4 * q + h, w[0], w[1], w[2], w[3]);
+            for (int u = 0; u < NIT; ++u) {
+                const int it = tid + u * G::THREADS;
+                const int slot = it & (G::NSLOT - 1), q = it / G::NSLOT;
+                const int w1 = slot / H2, pw = slot & (H2 - 1);
+                const uint8_t *ra = vb + (long long)w1 * o.sx + (long long)pw * o.sy + 16 * q;
+                a[u] = make_uint4(0u, 0u, 0u, 0u);
+                b[u] = a[u];
+                if (it < G::NSLOT * NQ && (unsigned)(z0 + 16 * q) < (unsigned)N) {
+                    a[u] = __ldg(reinterpret_cast<const uint4 *>(ra));
+                    b[u] = __ldg(reinterpret_cast<const uint4 *>(ra + (long long)H2 * o.sy));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < NIT; ++u) {
+                const int it = tid + u * G::THREADS;
+                if (it < G::NSLOT * NQ) {
+                    const int slot = it & (G::NSLOT - 1), q = it / G::NSLOT;
+                    const uint32_t av[4] = {a[u].x, a[u].y, a[u].z, a[u].w}, bv[4] = {b[u].x, b[u].y, b[u].z, b[u].w};
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        uint32_t w[4];
+                        pair_bytes(av[h], bv[h], w);
+                        put4(slot, 4 * q + h, w[0], w[1], w[2], w[3]);
+                    }
                 }
             }
         } else if (K == 4 && p.vec_ok && o.fast == 1) {
             // y' contiguous: one LDG.128 along y' = all 16 w2 of (w1, z'); 4 consecutive z' per item
             const bool fwd = o.sy > 0;
-            constexpr int NE4 = BW / 4;
-            for (int it = tid; it < S * NE4; it += blockDim.x) {
-                const int w1 = it / NE4, e4 = it - w1 * NE4;
-                uint32_t wd[4][H2];
+            const uint8_t *vb = vox(xb, yb + (fwd ? 0 : 15), z0);
+            constexpr int NE4 = BW / 4, IT = 2;
+            for (int base = tid; base < S * NE4; base += IT * blockDim.x) {
+                uint4 v[IT][4];
 #pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const int z = z0 + 4 * e4 + t;
-                    uint4 v = make_uint4(0u, 0u, 0u, 0u);
-                    if ((unsigned)z < (unsigned)N)
-                        v = __ldg(reinterpret_cast<const uint4 *>(vox(xb + w1, yb + (fwd ? 0 : 15), z)));
-                    if (!fwd) v = rev16(v);                // byte b <-> w2 = b
-                    uint32_t lo[4], hi[4];
-                    pair_bytes(v.x, v.z, lo);              // w2 = 0..3 with 8..11
-                    pair_bytes(v.y, v.w, hi);              // w2 = 4..7 with 12..15
+                for (int u = 0; u < IT; ++u) {
+                    const int it = base + u * blockDim.x;
+                    const int w1 = it / NE4, e4 = it - w1 * NE4;
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        wd[t][j] = lo[j];
-                        wd[t][4 + j] = hi[j];
+                    for (int t = 0; t < 4; ++t) {
+                        const int z = z0 + 4 * e4 + t;
+                        v[u][t] = make_uint4(0u, 0u, 0u, 0u);
+                        if (it < S * NE4 && (unsigned)z < (unsigned)N)
+                            v[u][t] = __ldg(reinterpret_cast<const uint4 *>(vb + (long long)w1 * o.sx +
+                                                                            (long long)(4 * e4 + t) * o.sz));
                     }
                 }
 #pragma unroll
-                for (int pw = 0; pw < H2; ++pw) put4(w1 * H2 + pw, e4, wd[0][pw], wd[1][pw], wd[2][pw], wd[3][pw]);
+                for (int u = 0; u < IT; ++u) {
+                    const int it = base + u * blockDim.x;
+                    if (it >= S * NE4) break;
+                    const int w1 = it / NE4, e4 = it - w1 * NE4;
+                    uint32_t wd[4][H2];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const uint4 x = fwd ? v[u][t] : rev16(v[u][t]);   // byte b <-> w2 = b
+                        uint32_t lo[4], hi[4];
+                        pair_bytes(x.x, x.z, lo);          // w2 = 0..3 with 8..11
+                        pair_bytes(x.y, x.w, hi);          // w2 = 4..7 with 12..15
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            wd[t][j] = lo[j];
+                            wd[t][4 + j] = hi[j];
+                        }
+                    }
+#pragma unroll
+                    for (int pw = 0; pw < H2; ++pw) put4(w1 * H2 + pw, e4, wd[0][pw], wd[1][pw], wd[2][pw], wd[3][pw]);
+                }
             }
         } else if (K == 4 && p.vec_ok && o.fast == 0) {
             // x' contiguous: LDG.128 along x' = all 16 w1 of (w2, z'); rows pw and pw + 8
             const bool fwd = o.sx > 0;
+            const uint8_t *vb = vox(xb + (fwd ? 0 : 15), yb, z0);
             constexpr int NE4 = BW / 4;
             for (int it = tid; it < H2 * NE4; it += blockDim.x) {
                 const int pw = it / NE4, e4 = it - pw * NE4;
@@ -149,8 +182,9 @@ drt_first_swar_kernel(const DrtPass p) {
                     const int z = z0 + 4 * e4 + t;
                     uint4 a = make_uint4(0u, 0u, 0u, 0u), b = a;
                     if ((unsigned)z < (unsigned)N) {
-                        a = __ldg(reinterpret_cast<const uint4 *>(vox(xb + (fwd ? 0 : 15), yb + pw, z)));
-                        b = __ldg(reinterpret_cast<const uint4 *>(vox(xb + (fwd ? 0 : 15), yb + pw + H2, z)));
+                        const uint8_t *ra = vb + (long long)pw * o.sy + (long long)(4 * e4 + t) * o.sz;
+                        a = __ldg(reinterpret_cast<const uint4 *>(ra));
+                        b = __ldg(reinterpret_cast<const uint4 *>(ra + (long long)H2 * o.sy));
                     }
                     if (!fwd) {
                         a = rev16(a);
@@ -224,11 +258,9 @@ drt_first_swar_kernel(const DrtPass p) {
                     const uint32_t sel = h ? 0x7632u : 0x5410u;
 #pragma unroll
                     for (int r2 = 0; r2 < S; ++r2) {
-                        uint32_t w[R / 2];
+                        uint32_t *o = reinterpret_cast<uint32_t *>(sm + G::ORP * ((grp + h * H2) * S + r2)) + (R / 2) * run;
 #pragma unroll
-                        for (int i = 0; i < R / 2; ++i) w[i] = __byte_perm(acc[r2][2 * i], acc[r2][2 * i + 1], sel);
-                        *reinterpret_cast<uint4 *>(sm + G::ORP * ((grp + h * H2) * S + r2) + 2 * R * run) =
-                            make_uint4(w[0], w[1], w[2], w[3]);
+                        for (int i = 0; i < R / 2; ++i) o[i] = __byte_perm(acc[r2][2 * i], acc[r2][2 * i + 1], sel);
                     }
                 }
             }
@@ -236,37 +268,42 @@ drt_first_swar_kernel(const DrtPass p) {
         __syncthreads();
     }
 
-    // ---- copy-out: stage-K rows stored pre-shifted by rho (common.cuh).  Item (row, k): k = 0 is
-    // the tail of the chunk before the tile (tile elements [0, rho)), k >= 1 the chunk holding tile
-    // elements [8(k-1) + rho, 8k + rho) (a head store when it runs past the tile).
+    // ---- copy-out, one row per thread: stage-K rows stored pre-shifted by rho (common.cuh).
+    // Stored chunk k of the tile (elements d0 + 8k .. + 7) holds tile elements [8k + rho, 8k + rho + 8);
+    // the last one is a head store when rho > 0, and the chunk before the tile gets a tail store of
+    // tile elements [0, rho) (its head belongs to the previous tile).
     uint16_t *outp = reinterpret_cast<uint16_t *>(p.out);
     const long long out_inst = (long long)li * p.out_inst_stride;
     const int mK = (1 << p.next_k) - 1;
     const int wv1 = V1 & mK, wv2 = V2 & mK;
-    constexpr int NK = T / 8 + 1;
-    for (int it = tid; it < S * S * NK; it += blockDim.x) {
-        const int rr = it / NK, k = it - rr * NK;
-        const int r1 = rr / S, r2 = rr - r1 * S;
+    constexpr int NCK = T / 8;
+    for (int rr = tid; rr < S * S; rr += blockDim.x) {
+        const int r1 = rr >> K, r2 = rr & (S - 1);
         const int rho = (r1 * wv1 + r2 * wv2) & 7;
-        const int s0 = 8 * (k - 1) + rho;                 // first tile element of the chunk (k >= 1)
-        const int pc = d0 + 8 * (k - 1);                  // stored element index of the chunk
-        if (k == 0 ? (rho == 0 || d0 < 8) : (pc >= p.out_width)) continue;
         const long long row = ((((long long)r1 << K) + r2) << (2 * m)) + ((long long)V1 << m) + V2;
-        uint16_t *dst = outp + out_inst + row * p.out_pitch + pc;
-        const uint32_t *srow = reinterpret_cast<const uint32_t *>(sm + G::ORP * rr);
-        const int sw = (k == 0 ? rho - 8 : s0);           // tile element at chunk position 0
-        // words covering tile elements [sw, sw + 8); indices below 0 only feed masked positions
-        const int w0 = sw >> 1;
-        uint32_t w[5];
+        uint16_t *dst = outp + out_inst + row * p.out_pitch + d0;
+        const uint32_t *srow = reinterpret_cast<const uint32_t *>(sm + G::ORP * rr) + (rho >> 1);
+        const uint32_t sel = (rho & 1) ? 0x5432u : 0x3210u;
+        uint32_t w[4 * NCK + 1];                          // the row's words, loaded before any store
 #pragma unroll
-        for (int i = 0; i < 5; ++i) w[i] = srow[(w0 + i) & (G::ORW - 1)];
-        const uint32_t sel = (sw & 1) ? 0x5432u : 0x3210u;
-        uint32_t v[4];
+        for (int i = 0; i < 4 * NCK + 1; ++i) w[i] = srow[i];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) v[i] = __byte_perm(w[i], w[i + 1], sel);
-        if (k == 0) store_chunk_tail<2>(dst, v, rho);
-        else if (s0 + 8 > T) store_chunk_head<2>(dst, v, T - s0);
-        else *reinterpret_cast<uint4 *>(dst) = make_uint4(v[0], v[1], v[2], v[3]);
+        for (int k = 0; k < NCK; ++k) {
+            uint32_t v[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v[i] = __byte_perm(w[4 * k + i], w[4 * k + i + 1], sel);
+            if (d0 + 8 * k < p.out_width) {
+                if (k == NCK - 1) store_chunk_head<2>(dst + 8 * k, v, 8 - rho);
+                else *reinterpret_cast<uint4 *>(dst + 8 * k) = make_uint4(v[0], v[1], v[2], v[3]);
+            }
+        }
+        if (rho > 0 && d0 >= 8) {
+            // tile elements [0, rho) end the previous chunk: window (zeros, row words 0..3)
+            const uint32_t *r0 = reinterpret_cast<const uint32_t *>(sm + G::ORP * rr);
+            uint32_t tw[8] = {0u, 0u, 0u, 0u, r0[0], r0[1], r0[2], r0[3]}, v[4];
+            window_chunk<2>(tw, rho, 0, v);
+            store_chunk_tail<2>(dst - 8, v, rho);
+        }
     }
 }
 
