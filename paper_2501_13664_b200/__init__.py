@@ -15,7 +15,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdrt3d.so")
+LIB_PATH = os.environ.get("D3_LIB") or os.path.join(_HERE, "libdrt3d.so")
 
 DRT3D_OK, DRT3D_ERR_INVALID_ARG, DRT3D_ERR_UNSUPPORTED, DRT3D_ERR_WORKSPACE, DRT3D_ERR_CUDA = range(5)
 DRT3D_U8, DRT3D_I32, DRT3D_F32 = range(3)

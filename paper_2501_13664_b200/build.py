@@ -13,11 +13,15 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "build_obj")
-LIB = os.path.join(HERE, "libdrt3d.so")
+# D3_EXTRA_FLAGS / D3_VARIANT build an instrumented side library (libdrt3d_<variant>.so) for
+# debugging; the product library is always libdrt3d.so.
+VARIANT = os.environ.get("D3_VARIANT", "")
+OBJ = os.path.join(HERE, "build_obj" + ("_" + VARIANT if VARIANT else ""))
+LIB = os.path.join(HERE, "libdrt3d" + ("_" + VARIANT if VARIANT else "") + ".so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-         "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
+         "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include"), "-I" + CSRC] + \
+        os.environ.get("D3_EXTRA_FLAGS", "").split()
 
 
 def _sources():

@@ -134,6 +134,28 @@ __device__ __forceinline__ void store_chunk_tail(void *chunk, const uint32_t (&v
     if (tb & 8) *reinterpret_cast<uint2 *>(p + 8) = make_uint2(v[2], v[3]);
 }
 
+// ---------------------------------------------------------------------------
+// L2 residency.  The 2.4 GB output streams through the
+// 126 MB L2; the cube and the stage buffers (re-read by the next pass / the
+// next dodecant) are marked evict_last so the stream does not push them out.
+__device__ __forceinline__ uint64_t l2_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void st_hint_v4(void *p, uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d),
+                 "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ uint4 ld_hint_v4(const void *p, uint64_t pol) {
+    uint4 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+
 // streaming (evict-first) 16-byte global store for final outputs that are
 // never re-read by this call.
 __device__ __forceinline__ void st_cs_v4(void *p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {

@@ -60,6 +60,10 @@ __device__ __forceinline__ uint4 rev16(uint4 v) {
                       __byte_perm(v.x, 0, 0x0123));
 }
 
+#ifndef SWAR_FMA16
+#define SWAR_FMA16 0                                      // all adds IADD3 (measured fastest)
+#endif
+
 template <int K, int R, int T>
 __global__ void __launch_bounds__(SwarGeom<K, R, T>::THREADS) __maxnreg__((SwarGeom<K, R, T>::MAXREG))
 drt_first_swar_kernel(const DrtPass p) {
@@ -143,8 +147,7 @@ drt_first_swar_kernel(const DrtPass p) {
                         const int z = z0 + 4 * e4 + t;
                         v[u][t] = make_uint4(0u, 0u, 0u, 0u);
                         if (it < S * NE4 && (unsigned)z < (unsigned)N)
-                            v[u][t] = __ldg(reinterpret_cast<const uint4 *>(vb + (long long)w1 * o.sx +
-                                                                            (long long)(4 * e4 + t) * o.sz));
+                            v[u][t] = __ldg(reinterpret_cast<const uint4 *>(vb + (long long)w1 * o.sx + (long long)(4 * e4 + t) * o.sz));
                     }
                 }
 #pragma unroll
@@ -230,7 +233,7 @@ drt_first_swar_kernel(const DrtPass p) {
             for (int i = 0; i < S; ++i)
 #pragma unroll
                 for (int j = 0; j < R; ++j) acc[i][j] = 0u;
-            drt_accumulate<K, R, SP, false, uint32_t, false>(sm, step ? grp * S : grp, step ? 1 : H2, run * (R / 4),
+            drt_accumulate<K, R, SP, false, uint32_t, SWAR_FMA16>(sm, step ? grp * S : grp, step ? 1 : H2, run * (R / 4),
                                                              p.one, acc);
         }
         __syncthreads();

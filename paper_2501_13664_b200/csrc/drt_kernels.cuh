@@ -25,6 +25,10 @@
 #pragma once
 #include "common.cuh"
 
+#ifndef D3_PF_GROUPS
+#define D3_PF_GROUPS 0
+#endif
+
 namespace d3 {
 
 struct DrtPass {
@@ -95,7 +99,11 @@ __device__ __forceinline__ Acc add2(Acc acc, uint32_t x, uint32_t y, uint32_t on
     }
 }
 
-template <int K, int R, int SP, bool U16, class Acc, bool FMA_SPLIT = true>
+// FMA16 of every 16 output rows take their adds on the FMA pipe (evenly spread over r).
+__host__ __device__ constexpr bool fma_row(int r, int fma16) { return ((r + 1) * fma16) / 16 > (r * fma16) / 16; }
+
+// FMA16 = -1: the measured default, rows with r % 8 < 3 (3/8 of the rows).
+template <int K, int R, int SP, bool U16, class Acc, int FMA16 = -1>
 __device__ __forceinline__ void drt_accumulate(const unsigned char *__restrict__ sm, int slot0, int sstep, int c0,
                                                uint32_t one, Acc (&acc)[1 << K][R]) {
     constexpr int S = 1 << K;
@@ -137,7 +145,7 @@ __device__ __forceinline__ void drt_accumulate(const unsigned char *__restrict__
             static_for<0, S>([&](auto r_) {
                 constexpr int r = decltype(r_)::value;
                 constexpr int o0 = lk(K, r, a0), o1 = lk(K, r, a1);
-                constexpr bool fma = FMA_SPLIT && (r % 8) < 3;
+                constexpr bool fma = FMA16 < 0 ? (r % 8) < 3 : fma_row(r, FMA16);
 #pragma unroll
                 for (int j = 0; j < R; ++j) acc[r][j] = add2<Acc>(acc[r][j], b0[j + o0], b1[j + o1], one, fma);
             });
@@ -331,6 +339,22 @@ drt_pass_kernel(const DrtPass p) {
         const int nc = p.n - c;
         const long long rbase = (((long long)sg1 << c) + sg2) << (2 * nc);
         const int nchunk = p.in_width >> LOG_EPC;          // chunks per stored row (width = pitch)
+#if D3_PF_GROUPS > 0
+        // L2 prefetch: the first D tile of each group pulls the rows of the group D3_PF_GROUPS ahead
+        // (the tiles of one group run together; the intermediate may have left L2)
+        if (tile == 0 && tid < S) {
+            const int gp = g + D3_PF_GROUPS;
+            if (gp < (int)gridDim.y) {
+                const int mm = (1 << m) - 1;
+                const int pV2 = gp & mm, pV1 = (gp >> m) & mm, psig = gp >> (2 * m);
+                const long long prow = ((((long long)(psig >> c) << c) + (psig & ((1 << c) - 1))) << (2 * nc)) +
+                                       ((long long)((pV1 << K) + tid) << nc) + (pV2 << K);
+                const unsigned bytes = (unsigned)(S * p.in_pitch * (int)sizeof(In));
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(inb + prow * p.in_pitch), "r"(bytes)
+                             : "memory");
+            }
+        }
+#endif
         const int cb = (Dabs - p.in_base) >> LOG_EPC;      // exact: Dabs - in_base is a multiple of 16
         for (int it = tid; it < S * S * NCH; it += blockDim.x) {
             const int slot = it / NCH, q = it - slot * NCH;

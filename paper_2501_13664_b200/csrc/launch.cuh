@@ -1,8 +1,10 @@
 // launch.cuh -- kernel launch templates (tile shapes per radix) shared by
 // the per-dtype translation units k_*.cu.
 #pragma once
+#include <cstdlib>
 #include "dispatch.h"
 #include "drt_first_swar.cuh"
+#include "drt_final_pipe.cuh"
 
 namespace d3 {
 
@@ -24,6 +26,30 @@ template <> struct DrtTile<4> { static constexpr int R = 8, T = 64; };
 template <int K, class In, class Acc, class Out, bool FIRST, bool FINAL>
 drt3d_status launch_drt_k(const DrtPass &prm, int ninst, cudaStream_t st) {
     constexpr int R = DrtTile<K>::R, T = DrtTile<K>::T;
+    if constexpr (!FIRST && FINAL && K == 4 && std::is_same<In, uint16_t>::value && std::is_same<Out, uint32_t>::value) {
+        static const bool use_pipe = getenv("D3_PIPE") != nullptr;   // experiment: pipelined final pass
+        if (use_pipe && prm.layout == 0 && (prm.out_width / 48) * 48 == prm.out_width && ((prm.out_width / 48) & (prm.out_width / 48 - 1)) == 0) {
+            // u16 rows -> int32 stacked output: persistent warp-specialised pipeline (drt_final_pipe.cuh)
+            constexpr int TP = 48;                      // 4 X + 3 Y + 1 producer warps: 255 regs/thread
+            using PG = PipeGeom<K, R, TP>;
+            auto kern = drt_final_pipe_kernel<K, R, TP>;
+            static bool attr_ok = set_smem(kern, PG::SMEM);
+            if (!attr_ok) return DRT3D_ERR_CUDA;
+            static int nsm = [] {
+                int dev = 0, v = 0;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+                return v > 0 ? v : 148;
+            }();
+            const int ntiles_d = prm.out_width / TP;            // a power of two (checked above)
+            int log_ntd = 0;
+            while ((1 << log_ntd) < ntiles_d) ++log_ntd;
+            const long long total = (long long)ninst * (1LL << (2 * (prm.c + prm.m))) * ntiles_d;
+            const int grid = (int)(total < nsm ? total : nsm);
+            kern<<<grid, PG::THREADS, PG::SMEM, st>>>(prm, log_ntd, (int)total);
+            return DRT3D_OK;
+        }
+    }
     if constexpr (FIRST && !FINAL && K >= 3 && std::is_same<In, uint8_t>::value && std::is_same<Out, uint16_t>::value) {
         // u8 voxels -> u16 stage-K rows: packed 16-bit lanes (drt_first_swar.cuh)
         using SG = SwarGeom<K, R, T>;

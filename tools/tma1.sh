@@ -1,2 +1,3 @@
 cd $GRAFT_REPO_ROOT/tools
-( for a in "0 0 1" "0 1 1" "0 0 2" "8 0 1" "1 0 1" "2 0 1" "4 0 1" "-8 0 1" "-1 0 1" "100 0 1" "0 0 4"; do ./tma_probe $a; done ) > ../gpurun_out/tma_probe.txt 2>&1
+./tma_rows_bench 2 208 x 148 > ../gpurun_out/plain_mb.log 2>&1 && ncu --set full --clock-control none -k regex:k -s 1 -c 1 -o ../gpurun_out/prof_mb ./tma_rows_bench 2 208 x 148 > ../gpurun_out/ncu_mb.log 2>&1
+./tma_rows_bench 3 208 x 148 > ../gpurun_out/plain_mb3.log 2>&1 && ncu --set full --clock-control none -k regex:k -s 1 -c 1 -o ../gpurun_out/prof_mb3 ./tma_rows_bench 3 208 x 148 >> ../gpurun_out/ncu_mb.log 2>&1

@@ -13,7 +13,7 @@ static __device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_
 
 constexpr int BW = 96, ROWS = 256, W = 288;
 
-__device__ __forceinline__ int row_start(long long row) { return (int)((row * 37) % 300) - 30; }
+__device__ __forceinline__ int row_start(long long row) { return (((int)((row * 37) % 300) - 30) / 8) * 8; }
 
 template <int MODE>
 __global__ void k(const __grid_constant__ CUtensorMap tm, const uint16_t *src, int nrows_total, int sp,
@@ -53,6 +53,29 @@ __global__ void k(const __grid_constant__ CUtensorMap tm, const uint16_t *src, i
                     : "r"(su32(bar)), "r"(it & 1)
                     : "memory");
             }
+        } else if (MODE == 3) {
+            // plain LDG.128 -> STS.128 (4 loads in flight per thread)
+            const int NCH = BW / 8 + 1;
+            for (int base = tid; base < ROWS * NCH; base += 4 * blockDim.x) {
+                uint4 v[4];
+                int dsto[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = base + u * blockDim.x;
+                    dsto[u] = -1;
+                    v[u] = make_uint4(0, 0, 0, 0);
+                    if (i < ROWS * NCH) {
+                        const int r = i / NCH, c = i % NCH;
+                        const int st = row_start(row0 + r);
+                        const int cc = (st >> 3) + c;
+                        if (cc >= 0 && cc < W / 8) v[u] = __ldg(reinterpret_cast<const uint4 *>(src + (row0 + r) * W + cc * 8));
+                        dsto[u] = r * sp + 16 * c;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (dsto[u] >= 0) *reinterpret_cast<uint4 *>(sm + dsto[u]) = v[u];
+            }
         } else {
             // cp.async 16-byte chunks covering [st, st + BW) (aligned source chunks; no realign)
             const int NCH = BW / 8 + 1;
@@ -78,7 +101,7 @@ __global__ void k(const __grid_constant__ CUtensorMap tm, const uint16_t *src, i
                 const int j = row_start(row0 + r) + e;
                 uint16_t expect = (j >= 0 && j < W) ? src[(row0 + r) * W + j] : 0;
                 uint16_t got;
-                if (MODE == 2) {
+                if (MODE >= 2) {
                     const int st = row_start(row0 + r);
                     const int jj = j - ((st >> 3) << 3);
                     got = *reinterpret_cast<const uint16_t *>(sm + r * sp + 2 * jj);
@@ -95,7 +118,7 @@ __global__ void k(const __grid_constant__ CUtensorMap tm, const uint16_t *src, i
 
 int main(int argc, char **argv) {
     const int mode = atoi(argv[1]), sp = atoi(argv[2]);
-    const int nrows = 65536 * 4;
+    const int nrows = 65536;
     std::vector<uint16_t> h((size_t)nrows * W);
     for (size_t i = 0; i < h.size(); ++i) h[i] = (uint16_t)(i * 2654435761u >> 7);
     uint16_t *d;
@@ -115,10 +138,10 @@ int main(int argc, char **argv) {
     CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, d, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     const int smem = ROWS * sp + 64;
-    auto kern = mode == 0 ? k<0> : mode == 1 ? k<1> : k<2>;
+    auto kern = mode == 0 ? k<0> : mode == 1 ? k<1> : mode == 2 ? k<2> : k<3>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    const int grid = 296, iters = 40;
-    if (argc > 3) {   // explicit 1-CTA cluster launch
+    const int grid = (argc > 4) ? atoi(argv[4]) : 296, iters = 40;
+    if (argc > 3 && argv[3][0] == 'c') {   // explicit 1-CTA cluster launch
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
