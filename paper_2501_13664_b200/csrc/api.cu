@@ -95,6 +95,7 @@ struct Plan {
     int chunk;              // instances per chunk
     size_t buf_bytes;       // one intermediate buffer (chunk instances)
     int nbuf;
+    int nset;               // 2: consecutive chunks use alternate buffer sets (cross-stream overlap)
     size_t ws_bytes;
     int nlaunch;
 };
@@ -203,8 +204,9 @@ drt3d_status make_plan(int transform, int N, uint32_t mask, const drt3d_opts &o,
         P.nbuf = P.npass >= 3 ? 2 : 1;
         P.buf_bytes = ((per_inst * (size_t)P.chunk + 255) / 256) * 256;
     }
-    P.ws_bytes = P.buf_bytes * P.nbuf;
     const int nchunks = (P.inst + P.chunk - 1) / P.chunk;
+    P.nset = (transform == 0 && P.npass > 1 && nchunks > 1) ? 2 : 1;
+    P.ws_bytes = P.buf_bytes * P.nbuf * P.nset;
     P.nlaunch = nchunks * P.npass + ((o.layout == DRT3D_LAYOUT_MOSAIC) ? 4 : 0);
     return DRT3D_OK;
 }
@@ -215,7 +217,9 @@ struct Launcher {
     const drt3d_opts *o;
     int count = 0;
     template <class F>
-    drt3d_status run(int kind, F &&launch) {
+    drt3d_status run(int kind, F &&launch) { return run_on(stream, kind, launch); }
+    template <class F>
+    drt3d_status run_on(cudaStream_t stream, int kind, F &&launch) {
         cudaEvent_t *ev = o && o->events ? reinterpret_cast<cudaEvent_t *>(o->events) : nullptr;
         const bool rec = ev && count < o->max_events;
         if (rec) cudaEventRecord(ev[2 * count], stream);
@@ -292,6 +296,33 @@ struct L2Window {
     }
 };
 
+// Cross-stream overlap of consecutive chunks: the first pass of
+// chunk i+1 runs on the caller's stream while the later passes of chunk i run on an auxiliary
+// stream, so the two latency-bound kernels share the SMs.  One auxiliary stream and four
+// events per (host thread, device), created on first use; the caller's stream is joined
+// before drt3d_planes returns, so stream semantics for the caller are unchanged.
+struct Aux {
+    cudaStream_t a = nullptr;
+    cudaEvent_t start = nullptr, fdone = nullptr, cdone[2] = {nullptr, nullptr};
+    bool ok = false;
+};
+Aux *aux_for_current_device() {
+    thread_local Aux aux[16];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
+    Aux &x = aux[dev];
+    if (!x.ok) {
+        if (cudaStreamCreateWithFlags(&x.a, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+        bool e = cudaEventCreateWithFlags(&x.start, cudaEventDisableTiming) == cudaSuccess;
+        e = e && cudaEventCreateWithFlags(&x.fdone, cudaEventDisableTiming) == cudaSuccess;
+        e = e && cudaEventCreateWithFlags(&x.cdone[0], cudaEventDisableTiming) == cudaSuccess;
+        e = e && cudaEventCreateWithFlags(&x.cdone[1], cudaEventDisableTiming) == cudaSuccess;
+        if (!e) return nullptr;
+        x.ok = true;
+    }
+    return &x;
+}
+
 drt3d_status run_drt(const void *cube, uint32_t mask, void *out, const drt3d_opts &o, const Plan &P, void *ws,
                      cudaStream_t st) {
     L2Window l2w(st, ws, P.ws_bytes);
@@ -314,12 +345,27 @@ drt3d_status run_drt(const void *cube, uint32_t mask, void *out, const drt3d_opt
             ++j;
         }
     Launcher L{st, &o};
-    char *buf[2] = {reinterpret_cast<char *>(ws), reinterpret_cast<char *>(ws) + P.buf_bytes};
+    static const bool no_overlap = getenv("D3_NO_OVERLAP") != nullptr;
+    Aux *ax = (P.nset == 2 && !no_overlap) ? aux_for_current_device() : nullptr;
+    if (ax && cudaEventRecord(ax->start, st) == cudaSuccess && cudaStreamWaitEvent(ax->a, ax->start, 0) == cudaSuccess) {
+    } else {
+        ax = nullptr;
+    }
     const long long final_inst = (o.layout == DRT3D_LAYOUT_MOSAIC) ? 0 : (long long)P.N * P.N * 3 * P.N;
-    for (int i0 = 0; i0 < P.inst; i0 += P.chunk) {
+    int chunk_idx = 0;
+    for (int i0 = 0; i0 < P.inst; i0 += P.chunk, ++chunk_idx) {
         const int ninst = (P.inst - i0) < P.chunk ? (P.inst - i0) : P.chunk;
+        const int set = ax ? (chunk_idx & 1) : 0;
+        char *sb = reinterpret_cast<char *>(ws) + (size_t)set * P.buf_bytes * P.nbuf;
+        char *buf[2] = {sb, sb + P.buf_bytes};
+        if (ax && chunk_idx >= 2) cudaStreamWaitEvent(st, ax->cdone[set], 0);   // buffer set free again
         for (int p = 0; p < P.npass; ++p) {
             const bool first = p == 0, fin = p == P.npass - 1;
+            cudaStream_t ps = (ax && !first) ? ax->a : st;
+            if (ax && p == 1) {
+                cudaEventRecord(ax->fdone, st);
+                cudaStreamWaitEvent(ax->a, ax->fdone, 0);
+            }
             DrtPass prm = base;
             prm.c = P.cs[p];
             prm.m = P.n - P.cs[p + 1];
@@ -336,12 +382,18 @@ drt3d_status run_drt(const void *cube, uint32_t mask, void *out, const drt3d_opt
             prm.out_width = P.width[p + 1];
             prm.next_k = fin ? 0 : P.ks[p + 1];
             drt3d_status s = DRT3D_OK;
-            drt3d_status ls = L.run(first ? 0 : (fin ? 2 : 1), [&] {
-                s = dispatch_drt(o.in_dtype, P.ks[p], P.stor[p], P.stor[p + 1], first, fin, prm, ninst, st);
+            drt3d_status ls = L.run_on(ps, first ? 0 : (fin ? 2 : 1), [&] {
+                s = dispatch_drt(o.in_dtype, P.ks[p], P.stor[p], P.stor[p + 1], first, fin, prm, ninst, ps);
             });
             if (s != DRT3D_OK) return s;
             if (ls != DRT3D_OK) return ls;
         }
+        if (ax) cudaEventRecord(ax->cdone[set], ax->a);
+    }
+    if (ax) {
+        // join: the caller's stream waits for the last chunk on the auxiliary stream
+        if (cudaEventRecord(ax->cdone[0], ax->a) != cudaSuccess || cudaStreamWaitEvent(st, ax->cdone[0], 0) != cudaSuccess)
+            return DRT3D_ERR_CUDA;
     }
     if (o.layout == DRT3D_LAYOUT_MOSAIC) {
         // the 4 blocks of the 4x4 grid no dodecant occupies
