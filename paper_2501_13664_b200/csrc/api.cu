@@ -334,6 +334,7 @@ drt3d_status run_drt(const void *cube, uint32_t mask, void *out, const drt3d_opt
     base.layout = o.layout;
     base.vec_ok = (P.N >= 16) ? 1 : 0;
     base.one = 1;
+    base.inst_total = P.inst;
     int j = 0;
     for (int k = 0; k < 12; ++k)
         if ((mask >> k) & 1) {

@@ -23,7 +23,19 @@
 //   (base 2N, width N); the final stage is the stacked output out[s1][s2][D],
 //   D in [0, 3N), zero outside the support.
 #pragma once
+#include <cuda.h>
 #include "common.cuh"
+
+// -DD3_PROF_PASS: per-phase clock accounting of the u16 final pass (thread 0 of each CTA),
+// summed into d3_pass_prof[] (debug builds only)
+#ifdef D3_PROF_PASS
+__device__ unsigned long long d3_pass_prof[16];
+#define PP_MARK(i) pp_t[i] = clock64()
+#define PP_ADD(slot, a, b) do { if (pp_on) atomicAdd(&d3_pass_prof[slot], (unsigned long long)(pp_t[b] - pp_t[a])); } while (0)
+#else
+#define PP_MARK(i)
+#define PP_ADD(slot, a, b) do { } while (0)
+#endif
 
 #ifndef D3_PF_GROUPS
 #define D3_PF_GROUPS 0
@@ -44,6 +56,8 @@ struct DrtPass {
     int layout;                     // final pass: 0 stacked, 1 mosaic
     int vec_ok;                     // first pass: 16-byte chunked cube loads are aligned (N >= 16)
     int next_k;                     // non-final passes: radix bits of the pass that reads this output
+    int inst_total;                 // instances (cubes x dodecants) of the whole call
+    int tma_store;                  // final pass: emit the output tile with one TMA tensor store
     uint32_t one;                   // = 1; a runtime multiplier so some adds issue as IMAD (FMA pipe)
     Orient ori[kMaxDod];            // first pass: per-dodecant-slot orientation
     int8_t out_order[kMaxDod][2];   // mosaic: OutOrder[k][0..1]
@@ -73,7 +87,11 @@ struct DrtGeom {
     // two CTAs per SM: with W warps per CTA one SM sub-partition holds ceil(2W/4) warps of its
     // 16K-register file, which caps the registers per thread
     static constexpr int WARPS = THREADS / 32;
-    static constexpr int MAXREG0 = 16384 / (((2 * WARPS + 3) / 4) * 32) / 8 * 8;
+    // CTAS resident CTAs per SM (shared memory bound); with W warps per CTA one SM sub-partition
+    // holds ceil(CTAS W / 4) warps of its 16K-register file, which caps the registers per thread
+    static constexpr int CTAS0 = (227 * 1024) / (SMEM + 1024);
+    static constexpr int CTAS = CTAS0 < 1 ? 1 : (CTAS0 > 4 ? 4 : CTAS0);
+    static constexpr int MAXREG0 = 16384 / (((CTAS * WARPS + 3) / 4) * 32) / 8 * 8;
     static constexpr int MAXREG = MAXREG0 > 255 ? 255 : MAXREG0;
     static_assert(T % R == 0 && R % 8 == 0, "tile shape");
     static_assert((NRY - 1) * R + (R + H + 3) / 4 * 4 <= NRX * R, "y-step reads inside X");
@@ -163,7 +181,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
 
 template <int K, int R, int T, class In, class Acc, class Out, bool FIRST, bool FINAL>
 __global__ void __maxnreg__((DrtGeom<K, R, T, !FIRST && sizeof(In) == 2>::MAXREG))
-drt_pass_kernel(const DrtPass p) {
+drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
     constexpr bool STAGE16 = !FIRST && sizeof(In) == 2;
     using G = DrtGeom<K, R, T, STAGE16>;
     constexpr int S = G::S, SP = G::SP, BW = G::BW;
@@ -235,6 +253,11 @@ drt_pass_kernel(const DrtPass p) {
         }
     }
 
+#ifdef D3_PROF_PASS
+    const bool pp_on = tid == 0 && STAGE16 && FINAL;
+    long long pp_t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
+    PP_MARK(0);
     // ---- stage the 4^K input rows of the group (32-bit lanes, BW elements per slot)
     auto put = [&](int slot, int e, uint32_t bits) {
         *reinterpret_cast<uint32_t *>(sm + slot * SP + 16 * xswz(e >> 2) + 4 * (e & 3)) = bits;
@@ -366,9 +389,11 @@ drt_pass_kernel(const DrtPass p) {
             unsigned char *dst = sm + slot * SP + 16 * (STAGE16 ? q : xswz(q));
             cp_async16(dst, ok ? (const void *)src : (const void *)inb, ok);
         }
+        PP_MARK(1);
         cp_async_wait_all();
     }
     __syncthreads();
+    PP_MARK(2);
 
     // ---- x-step (rows w1 of slot (w1, w2) -> X(r1, w2)), written in place over slot (r1, w2),
     // then y-step (rows w2 of X slot (r1, w2) -> out(r1, r2)); one code path, two iterations.
@@ -397,13 +422,17 @@ drt_pass_kernel(const DrtPass p) {
             zero_acc();
             drt_accumulate<K, R, SP, true, Acc>(sm, xb, S, xr * (R / 8), p.one, acc);
         }
+        PP_MARK(3);
         __syncthreads();
+        PP_MARK(4);
         if (tid < G::XT) write_x();
         __syncthreads();
+        PP_MARK(5);
         if (tid < G::YT) {
             zero_acc();
             drt_accumulate<K, R, SP, false, Acc>(sm, yb * S, 1, yr * (R / 4), p.one, acc);
         }
+        PP_MARK(6);
     } else {
         // both steps read 32-bit rows: one code path, two iterations
 #pragma unroll 1
@@ -472,6 +501,36 @@ drt_pass_kernel(const DrtPass p) {
         return;
     }
 
+    // ---- final output via SMEM + one TMA tensor store (stacked layout, m = 0): the tile is the
+    // box {T, S (s2), S (s1), 1} of out[inst][s1][s2][3N]
+    if constexpr (FINAL && sizeof(Out) == 4) {
+        if (p.tma_store) {
+            __syncthreads();                                 // every y-step read of X is done
+            if (tid < G::YT) {
+                unsigned char *row = sm + ((yb * S) * T + yr * R) * 4;
+#pragma unroll
+                for (int r2 = 0; r2 < S; ++r2)
+#pragma unroll
+                    for (int q = 0; q < R / 4; ++q)
+                        *reinterpret_cast<uint4 *>(row + (r2 * T + 4 * q) * 4) =
+                            make_uint4(Lane<Acc>::bits(acc[r2][4 * q]), Lane<Acc>::bits(acc[r2][4 * q + 1]),
+                                       Lane<Acc>::bits(acc[r2][4 * q + 2]), Lane<Acc>::bits(acc[r2][4 * q + 3]));
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            if (tid == 0) {
+                const uint32_t src = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+                asm volatile(
+                    "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(&omap),
+                    "r"(d0), "r"(sg2 << K), "r"(sg1 << K), "r"(inst), "r"(src)
+                    : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            }
+            return;
+        }
+    }
+
     // ---- store out(r1 = yb, r2, run yr)
     if (tid < G::YT) {
         const int r1 = yb, e0 = yr * R;
@@ -514,6 +573,19 @@ drt_pass_kernel(const DrtPass p) {
             }
         }
     }
+#ifdef D3_PROF_PASS
+    if constexpr (STAGE16 && FINAL) {
+        PP_MARK(7);
+        PP_ADD(0, 0, 1);    // staging issue
+        PP_ADD(1, 1, 2);    // staging wait + barrier
+        PP_ADD(2, 2, 3);    // x-step
+        PP_ADD(3, 3, 4);    // barrier after x
+        PP_ADD(4, 4, 5);    // write X + barrier
+        PP_ADD(5, 5, 6);    // y-step
+        PP_ADD(6, 6, 7);    // stores
+        if (pp_on) atomicAdd(&d3_pass_prof[7], 1ull);
+    }
+#endif
 }
 
 }  // namespace d3

@@ -2,6 +2,8 @@
 // the per-dtype translation units k_*.cu.
 #pragma once
 #include <cstdlib>
+#include <cstring>
+#include <cudaTypedefs.h>
 #include "dispatch.h"
 #include "drt_first_swar.cuh"
 #include "drt_final_pipe.cuh"
@@ -23,9 +25,40 @@ template <> struct DrtTile<2> { static constexpr int R = 8, T = 128; };
 template <> struct DrtTile<3> { static constexpr int R = 8, T = 64; };
 template <> struct DrtTile<4> { static constexpr int R = 8, T = 64; };
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+inline PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &f, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }();
+    return fn;
+}
+
+// 4D map of the stacked DRT output out[inst][s1][s2][3N] (32-bit), box {T, S, S, 1}
+inline bool make_out_map(CUtensorMap *m, void *out, int N, int inst_total, int T, int S) {
+    auto enc = tmap_encoder();
+    if (!enc) return false;
+    const cuuint64_t W = 3ull * N;
+    cuuint64_t dims[4] = {W, (cuuint64_t)N, (cuuint64_t)N, (cuuint64_t)inst_total};
+    cuuint64_t str[3] = {W * 4, W * 4 * N, W * 4 * N * N};
+    cuuint32_t box[4] = {(cuuint32_t)T, (cuuint32_t)S, (cuuint32_t)S, 1}, es[4] = {1, 1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, out, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+           CUDA_SUCCESS;
+}
+
 template <int K, class In, class Acc, class Out, bool FIRST, bool FINAL>
-drt3d_status launch_drt_k(const DrtPass &prm, int ninst, cudaStream_t st) {
-    constexpr int R = DrtTile<K>::R, T = DrtTile<K>::T;
+drt3d_status launch_drt_k(const DrtPass &prm_in, int ninst, cudaStream_t st) {
+    DrtPass prm = prm_in;
+#ifndef D3_FINAL16_T
+#define D3_FINAL16_T 64
+#endif
+    // u16-input passes may use a narrower tile (more resident CTAs per SM)
+    constexpr int R = DrtTile<K>::R, T = (!FIRST && sizeof(In) == 2 && K == 4) ? D3_FINAL16_T : DrtTile<K>::T;
     if constexpr (!FIRST && FINAL && K == 4 && std::is_same<In, uint16_t>::value && std::is_same<Out, uint32_t>::value) {
         static const bool use_pipe = getenv("D3_PIPE") != nullptr;   // experiment: pipelined final pass
         if (use_pipe && prm.layout == 0 && (prm.out_width / 48) * 48 == prm.out_width && ((prm.out_width / 48) & (prm.out_width / 48 - 1)) == 0) {
@@ -69,7 +102,17 @@ drt3d_status launch_drt_k(const DrtPass &prm, int ninst, cudaStream_t st) {
     const int ntiles = (prm.out_width + (FINAL ? 0 : 16 / (int)sizeof(Out)) + T - 1) / T;
     const long long groups = 1LL << (2 * (prm.c + prm.m));
     dim3 grid(ntiles, (unsigned)groups, ninst);
-    kern<<<grid, G::THREADS, G::SMEM, st>>>(prm);
+    CUtensorMap omap;
+    std::memset(&omap, 0, sizeof(omap));
+    prm.tma_store = 0;
+    static const bool no_tma = getenv("D3_NO_TMA_STORE") != nullptr;
+    if constexpr (FINAL && sizeof(Out) == 4) {
+        constexpr int S = 1 << K;
+        if (!no_tma && prm.layout == 0 && prm.m == 0 && prm.out_width % T == 0 && S * S * T * 4 <= G::SMEM &&
+            make_out_map(&omap, prm.out, prm.N, prm.inst_total, T, S))
+            prm.tma_store = 1;
+    }
+    kern<<<grid, G::THREADS, G::SMEM, st>>>(prm, omap);
     return DRT3D_OK;
 }
 
