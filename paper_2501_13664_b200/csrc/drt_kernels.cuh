@@ -379,15 +379,23 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
         }
 #endif
         const int cb = (Dabs - p.in_base) >> LOG_EPC;      // exact: Dabs - in_base is a multiple of 16
-        for (int it = tid; it < S * S * NCH; it += blockDim.x) {
-            const int slot = it / NCH, q = it - slot * NCH;
-            const int w1 = slot >> K, w2 = slot & (S - 1);
-            const long long row = rbase + ((long long)((V1 << K) + w1) << nc) + (V2 << K) + w2;
-            const int cc = cb + ((sg1 * w1 + sg2 * w2) >> LOG_EPC) + q;
-            const bool ok = (unsigned)cc < (unsigned)nchunk;
-            const uint4 *src = reinterpret_cast<const uint4 *>(inb + row * p.in_pitch) + cc;
-            unsigned char *dst = sm + slot * SP + 16 * (STAGE16 ? q : xswz(q));
-            cp_async16(dst, ok ? (const void *)src : (const void *)inb, ok);
+        // thread (sub, q) copies chunk q of slots sub, sub + SUBS, ...: the per-copy work is the
+        // slot's shift term and one address add
+        constexpr int SUBS = G::THREADS / NCH;             // slots in flight per iteration
+        const int q = tid % NCH, sub = tid / NCH;
+        if (sub < SUBS) {
+            const In *rb = inb + (rbase + ((long long)(V1 << K) << nc) + (V2 << K)) * p.in_pitch;
+            unsigned char *dst = sm + sub * SP + 16 * (STAGE16 ? q : xswz(q));
+            const int cq = cb + q;
+#pragma unroll 4
+            for (int slot = sub; slot < S * S; slot += SUBS, dst += SUBS * SP) {
+                const int w1 = slot >> K, w2 = slot & (S - 1);
+                const int cc = cq + ((sg1 * w1 + sg2 * w2) >> LOG_EPC);
+                const bool ok = (unsigned)cc < (unsigned)nchunk;
+                const uint32_t off = ((uint32_t)((w1 << nc) + w2) * (uint32_t)p.in_pitch + (uint32_t)(ok ? cc : 0) * EPC) *
+                                     (uint32_t)sizeof(In);
+                cp_async16(dst, reinterpret_cast<const char *>(rb) + off, ok);
+            }
         }
         PP_MARK(1);
         cp_async_wait_all();
