@@ -535,6 +535,19 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             }
+#ifdef D3_PROF_PASS
+            if constexpr (STAGE16) {
+                PP_MARK(7);
+                PP_ADD(0, 0, 1);
+                PP_ADD(1, 1, 2);
+                PP_ADD(2, 2, 3);
+                PP_ADD(3, 3, 4);
+                PP_ADD(4, 4, 5);
+                PP_ADD(5, 5, 6);
+                PP_ADD(6, 6, 7);
+                if (pp_on) atomicAdd(&d3_pass_prof[7], 1ull);
+            }
+#endif
             return;
         }
     }

@@ -1,0 +1,3 @@
+cd $GRAFT_REPO_ROOT
+bash tools/cycle.sh r1x
+D3_NO_OVERLAP=1 timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/bench_r1x_noov.log 2>&1
