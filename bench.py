@@ -99,6 +99,23 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+# ------------------------------------------------------------ multi-rank plumbing
+def max_over_ranks(x: float, world: int, device=None) -> float:
+    """Max of a per-rank scalar over all ranks (timing rule: max over ranks)."""
+    if world <= 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_gvoxels(units_per_rank: float, world: int, ms_per_step: float) -> float:
+    """Whole-job throughput: every rank transforms its own cube (weak scaling)."""
+    return world * units_per_rank / (ms_per_step * 1e-3) / 1e9
+
+
 # ------------------------------------------------------------ CPU oracle arm
 def _oracle_dodecant(k: int) -> float:
     import numpy as np
@@ -237,13 +254,9 @@ def run_ours(args):
         dist.barrier()
     clocks = sampler.stop()
     step_ms = [a.elapsed_time(b) for a, b in zip(starts, stops)]
-    tot_ms = sum(step_ms)
-    if world > 1:
-        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot_ms = float(t.item())
+    tot_ms = max_over_ranks(sum(step_ms), world, dev)
     ms_per_step = tot_ms / args.steps
-    value = world * N ** 3 / (ms_per_step * 1e-3) / 1e9            # Gvoxel/s, whole job
+    value = whole_job_gvoxels(N ** 3, world, ms_per_step)          # Gvoxel/s, whole job
 
     peak, peak_kind = _peaks()
     # algorithmic bytes: whole call = cube read once + output written once
@@ -254,6 +267,14 @@ def run_ours(args):
     fin_ms = statistics.mean(kind_ms[2]) if kind_ms[2] else float("nan")
     first_ms = statistics.mean(kind_ms[0]) if kind_ms[0] else float("nan")
     achieved = final_bytes / (fin_ms * 1e-3) / 1e9
+    # dram__bytes_read.sum + dram__bytes_write.sum of the final pass from the committed ncu --set full
+    # capture (profiles/ncu_traffic.json, written by tools/ncu_traffic.py from that report)
+    traffic, traffic_src = None, None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            tj = json.load(fh)
+        traffic, traffic_src = tj.get("final_pass_dram_bytes_per_launch"), tj.get("source")
     share = sum(kind_ms[2]) / max(1e-9, sum(kind_ms[0]) + sum(kind_ms[1]) + sum(kind_ms[2]))
 
     # e2e through the host-buffer C entry point (pinned host cube + output)
@@ -277,14 +298,10 @@ def run_ours(args):
             e2e_step()
         b.record(stream)
         torch.cuda.synchronize()
-        e_ms = a.elapsed_time(b) / args.e2e_steps
-        if world > 1:
-            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = float(t.item())
+        e_ms = max_over_ranks(a.elapsed_time(b) / args.e2e_steps, world, dev)
         # spot-check that the e2e result is the device result
         assert bool((hout[0, 0, 0, 0].to(dev) == out[0, 0, 0, 0]).all())
-        e2e = {"value": world * N ** 3 / (e_ms * 1e-3) / 1e9, "unit": "Gvoxel/s", "ms_per_step": e_ms,
+        e2e = {"value": whole_job_gvoxels(N ** 3, world, e_ms), "unit": "Gvoxel/s", "ms_per_step": e_ms,
                "h2d_bytes_per_step": int(cube.numel()), "d2h_bytes_per_step": int(out.numel() * 4)}
 
     cpu = None
@@ -310,7 +327,8 @@ def run_ours(args):
             "call_frac_of_peak": call_bytes / (ms_per_step * 1e-3) / 1e9 / peak,
             "roofline": {"kernel": "drt_pass_kernel<K=4> final pass", "bound": "hbm", "achieved": achieved,
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "algorithmic_bytes_per_launch": final_bytes,
+                         "traffic": traffic, "traffic_source": traffic_src,
+                         "algorithmic_bytes_per_launch": final_bytes,
                          "launch_ms": fin_ms, "first_pass_ms": first_ms, "share_of_step": share},
             "gpu_launches": launches,
             "clocks": clocks,
