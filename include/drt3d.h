@@ -10,8 +10,12 @@
  * ----------------------------------
  *  - All data pointers (`cube`, `out`, `workspace`) are DEVICE pointers unless
  *    the function name ends in `_host`.  The caller owns every buffer; the
- *    library never allocates, frees, or synchronises, and enqueues its kernels
- *    on `stream` (a cudaStream_t passed as void*, NULL = legacy default stream).
+ *    library never allocates device memory, frees, or synchronises, and enqueues
+ *    its kernels on `stream` (a cudaStream_t passed as void*, NULL = legacy
+ *    default stream).  Multi-chunk DRT calls may also run passes on an internal
+ *    auxiliary stream (one per host thread and device, created on first use) that
+ *    is forked from and joined back into `stream` within the call, so ordering
+ *    with respect to `stream` is unchanged.
  *  - N must be a power of two, 2 <= N <= 1024 (non-cubic / non-dyadic volumes are
  *    out of scope).
  *  - cube layout: C order [batch][x][y][z], z fastest; element type opts->in_dtype.
