@@ -60,6 +60,14 @@ __device__ __forceinline__ uint4 rev16(uint4 v) {
                       __byte_perm(v.x, 0, 0x0123));
 }
 
+// -DD3_PROF_SWAR: per-phase clock accounting (thread 0 of each CTA) into d3_swar_prof[]
+#ifdef D3_PROF_SWAR
+__device__ unsigned long long d3_swar_prof[16];
+#define SW_MARK(i) sw_t[i] = clock64()
+#else
+#define SW_MARK(i)
+#endif
+
 #ifndef SWAR_FMA16
 #define SWAR_FMA16 0                                      // all adds IADD3 (measured fastest)
 #endif
@@ -82,6 +90,10 @@ drt_first_swar_kernel(const DrtPass p) {
     const int Dabs = p.out_base + d0;
     const int N = p.N;
 
+#ifdef D3_PROF_SWAR
+    long long sw_t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
+    SW_MARK(0);
     auto put4 = [&](int slot, int chunk, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
         *reinterpret_cast<uint4 *>(sm + slot * SP + 16 * xswz(chunk)) = make_uint4(a, b, c, d);
     };
@@ -218,6 +230,7 @@ drt_first_swar_kernel(const DrtPass p) {
         }
     }
     __syncthreads();
+    SW_MARK(1);
 
     // ---- x-step on (w2, w2 + H2) pairs, then y-step on (r1, r1 + H2) pairs; one code path.
     //   step 0: thread (pw, run)  -> acc[r1][j] = (X(r1, pw), X(r1, pw + H2))
@@ -236,6 +249,9 @@ drt_first_swar_kernel(const DrtPass p) {
             drt_accumulate<K, R, SP, false, uint32_t, SWAR_FMA16>(sm, step ? grp * S : grp, step ? 1 : H2, run * (R / 4),
                                                              p.one, acc);
         }
+#ifdef D3_PROF_SWAR
+        if (step == 0) SW_MARK(2); else SW_MARK(4);
+#endif
         __syncthreads();
         if (act) {
             if (step == 0) {
@@ -269,6 +285,9 @@ drt_first_swar_kernel(const DrtPass p) {
             }
         }
         __syncthreads();
+#ifdef D3_PROF_SWAR
+        if (step == 0) SW_MARK(3); else SW_MARK(5);
+#endif
     }
 
     // ---- copy-out, one row per thread: stage-K rows stored pre-shifted by rho (common.cuh).
@@ -308,6 +327,13 @@ drt_first_swar_kernel(const DrtPass p) {
             store_chunk_tail<2>(dst - 8, v, rho);
         }
     }
+#ifdef D3_PROF_SWAR
+    SW_MARK(6);
+    if (tid == 0) {
+        for (int i = 0; i < 6; ++i) atomicAdd(&d3_swar_prof[i], (unsigned long long)(sw_t[i + 1] - sw_t[i]));
+        atomicAdd(&d3_swar_prof[7], 1ull);
+    }
+#endif
 }
 
 }  // namespace d3

@@ -30,3 +30,11 @@ extern "C" int d3_pass_prof_read(unsigned long long *out16) {
     return cudaMemcpyToSymbol(d3_pass_prof, z, sizeof(z)) != cudaSuccess;
 }
 #endif
+
+#ifdef D3_PROF_SWAR
+extern "C" int d3_swar_prof_read(unsigned long long *out16) {
+    if (cudaMemcpyFromSymbol(out16, d3::d3_swar_prof, 16 * sizeof(unsigned long long)) != cudaSuccess) return 1;
+    unsigned long long z[16] = {0};
+    return cudaMemcpyToSymbol(d3::d3_swar_prof, z, sizeof(z)) != cudaSuccess;
+}
+#endif
