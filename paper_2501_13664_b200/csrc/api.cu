@@ -100,7 +100,13 @@ struct Plan {
     int nlaunch;
 };
 
-const size_t kChunkBudget = 64ull << 20;   // keep a chunk's intermediates L2-resident (126 MB L2)
+#ifndef D3_CHUNK_MB
+#define D3_CHUNK_MB 512
+#endif
+// Intermediates per chunk.  Large chunks win (measured): one first-pass launch over
+// many dodecants re-reads the cube from L2 and neither launch has a partial last wave; the stage
+// buffers then live in HBM (they do not stay in L2 under the output stream anyway).
+const size_t kChunkBudget = (size_t)D3_CHUNK_MB << 20;
 
 int ilog2_exact(int N) {
     if (N < 2 || N > 1024) return -1;

@@ -58,9 +58,10 @@ def test_workspace_sizes():
     o = d3.make_opts()
     assert d3.drt3d_planes_workspace_size(16, 0x1, o) == 0  # single pass, no intermediate
     ws = d3.drt3d_planes_workspace_size(256, 0xFFF, o)
-    # one N=256 dodecant's stage-4 buffer: N^2 rows x pitch 288 x u16
-    assert ws >= 256 * 256 * 288 * 2
-    assert ws < 200 << 20
+    # N=256, 12 dodecants in one chunk: 12 stage-4 buffers of N^2 rows x u16, pitch
+    # round16(3N - base) with base = floor16(2N - 2 (2^4 - 1) - 7) = 464 -> 304
+    assert ws == 12 * 256 * 256 * 304 * 2
+    assert ws <= 512 << 20
     assert d3.djt3d_lines_workspace_size(64, 0x1, o) > 0
 
 
