@@ -120,7 +120,7 @@ __device__ __forceinline__ Acc add2(Acc acc, uint32_t x, uint32_t y, uint32_t on
 // FMA16 of every 16 output rows take their adds on the FMA pipe (evenly spread over r).
 __host__ __device__ constexpr bool fma_row(int r, int fma16) { return ((r + 1) * fma16) / 16 > (r * fma16) / 16; }
 
-// FMA16 = -1: the measured default, rows with r % 8 < 3 (3/8 of the rows).
+// FMA16 = -1: the measured default, rows with r % 4 < 1 (1/4 of the rows; swept 0 .. 3/8).
 template <int K, int R, int SP, bool U16, class Acc, int FMA16 = -1>
 __device__ __forceinline__ void drt_accumulate(const unsigned char *__restrict__ sm, int slot0, int sstep, int c0,
                                                uint32_t one, Acc (&acc)[1 << K][R]) {
@@ -163,7 +163,11 @@ __device__ __forceinline__ void drt_accumulate(const unsigned char *__restrict__
             static_for<0, S>([&](auto r_) {
                 constexpr int r = decltype(r_)::value;
                 constexpr int o0 = lk(K, r, a0), o1 = lk(K, r, a1);
-                constexpr bool fma = FMA16 < 0 ? (r % 8) < 3 : fma_row(r, FMA16);
+#ifndef D3_FMA_MOD
+#define D3_FMA_MOD 4
+#define D3_FMA_LT 1
+#endif
+                constexpr bool fma = FMA16 < 0 ? (r % D3_FMA_MOD) < D3_FMA_LT : fma_row(r, FMA16);
 #pragma unroll
                 for (int j = 0; j < R; ++j) acc[r][j] = add2<Acc>(acc[r][j], b0[j + o0], b1[j + o1], one, fma);
             });
