@@ -156,6 +156,15 @@ __device__ __forceinline__ uint4 ld_hint_v4(const void *p, uint64_t pol) {
     return v;
 }
 
+// Task -> (row, run) with quarter-warps on 8 consecutive runs of one row (conflict-free
+// 16-byte shared loads): tasks below 8 * nrows cover runs 0..7, the rest runs 8..nr-1.
+__device__ __forceinline__ void task_row_run(int t, int nr, int nrows, int &row, int &run) {
+    if (nr <= 8 || t < 8 * nrows) { row = t >> 3; run = t & 7; if (nr < 8) { row = t / nr; run = t - row * nr; } return; }
+    const int u = t - 8 * nrows, extra = nr - 8;
+    row = u / extra;
+    run = 8 + (u - row * extra);
+}
+
 // streaming (evict-first) 16-byte global store for final outputs that are
 // never re-read by this call.
 __device__ __forceinline__ void st_cs_v4(void *p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {

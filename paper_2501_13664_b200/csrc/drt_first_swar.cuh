@@ -40,10 +40,13 @@ struct SwarGeom {
     static constexpr int ORP = (ORW + 1) * 4;             // odd word pitch: rows hit distinct banks
     static constexpr int SMEM0 = NSLOT * SP;
     static constexpr int SMEM = (SMEM0 > S * S * ORP ? SMEM0 : S * S * ORP);
-    static constexpr int CTAS = 4;                        // target CTAs per SM
+#ifndef SWAR_CTAS
+#define SWAR_CTAS 4
+#endif
+    static constexpr int CTAS = SWAR_CTAS;                // target CTAs per SM (register cap)
     static constexpr int MAXREG0 = 65536 / (CTAS * THREADS) / 8 * 8;
     static constexpr int MAXREG = MAXREG0 > 255 ? 255 : MAXREG0;
-    static_assert(T % R == 0 && R == 8, "tile shape");
+    static_assert(T % R == 0 && (R == 8 || R == 4), "tile shape");
     static_assert(NRY == 8 || NRY == 16, "y runs per row must be a shuffle width");
 };
 
@@ -238,8 +241,8 @@ drt_first_swar_kernel(const DrtPass p) {
     uint32_t acc[S][R];
 #pragma unroll 1
     for (int step = 0; step < 2; ++step) {
-        const int nr = step ? G::NRY : G::NRX;
-        const int grp = tid / nr, run = tid - grp * nr;
+        int grp, run;
+        task_row_run(tid, step ? G::NRY : G::NRX, H2, grp, run);
         const bool act = tid < (step ? G::YT : G::XT);
         if (act) {
 #pragma unroll

@@ -410,7 +410,8 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
     // ---- x-step (rows w1 of slot (w1, w2) -> X(r1, w2)), written in place over slot (r1, w2),
     // then y-step (rows w2 of X slot (r1, w2) -> out(r1, r2)); one code path, two iterations.
     Acc acc[S][R];
-    const int xr = tid % G::NRX, xb = tid / G::NRX;
+    int xb, xr;
+    task_row_run(tid, G::NRX, S, xb, xr);
     const int yr = tid % G::NRY, yb = tid / G::NRY;
     auto zero_acc = [&]() {
 #pragma unroll

@@ -112,8 +112,12 @@ drt3d_status launch_drt_k(const DrtPass &prm_in, int ninst, cudaStream_t st) {
     }
     if constexpr (FIRST && !FINAL && K >= 3 && std::is_same<In, uint8_t>::value && std::is_same<Out, uint16_t>::value) {
         // u8 voxels -> u16 stage-K rows: packed 16-bit lanes (drt_first_swar.cuh)
-        using SG = SwarGeom<K, R, T>;
-        auto kern = drt_first_swar_kernel<K, R, T>;
+#ifndef SWAR_R
+#define SWAR_R 8
+#endif
+        constexpr int RS = SWAR_R;
+        using SG = SwarGeom<K, RS, T>;
+        auto kern = drt_first_swar_kernel<K, RS, T>;
         static bool attr_ok = set_smem(kern, SG::SMEM);
         if (!attr_ok) return DRT3D_ERR_CUDA;
         const int ntiles = (prm.out_width + 8 + T - 1) / T;
