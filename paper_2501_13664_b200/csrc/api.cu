@@ -173,12 +173,17 @@ drt3d_status make_plan(int transform, int N, uint32_t mask, const drt3d_opts &o,
             if (p == P.npass) { P.base[p] = 0; P.width[p] = 3 * N; P.pitch[p] = 3 * N; }
             else {
                 // stage-c support starts at D = 2N - 2(2^c - 1) (eq:3Dfm).  Rows are
-                // stored pre-shifted left by rho < 8 elements,
-                // so the stored origin sits at least 7 below the support, rounded down to 16 so
-                // that every reader window starts on a 16-byte chunk; rows are computed
-                // (zero-padded) up to their pitch so any 16-byte chunk inside a row is valid data.
-                P.base[p] = (2 * N - 2 * ((1 << c) - 1) - 7) / 16 * 16;
-                P.pitch[p] = round_up(3 * N - P.base[p], 16);
+                // stored pre-shifted left by rho < EPC elements (DESIGN.md "Aligned stage buffers",
+                // EPC = elements per 16-byte chunk), so the stored origin sits at least EPC - 1 below
+                // the support, rounded down to a chunk so that every reader window starts on one;
+                // the pitch is a whole number of chunks and rows are computed (zero-padded) up to
+                // it, so any chunk inside a row is valid data.
+                // (u16 stages keep a 16-element origin: the first pass's vector cube loads along z'
+                // need z' = D - 2N to start on 16 bytes.)
+                const int epc = 16 / stor_bytes(P.stor[p]);
+                const int gb = P.stor[p] == ST_U16 ? 16 : epc;
+                P.base[p] = (2 * N - 2 * ((1 << c) - 1) - (epc - 1)) / gb * gb;
+                P.pitch[p] = round_up(3 * N - P.base[p], epc);
                 P.width[p] = P.pitch[p];
             }
             P.inst_elems[p] = (long long)N * N * P.pitch[p];

@@ -1,0 +1,71 @@
+"""Secondary measurement: every BASELINE.json config through the C ABI on one B200.
+
+Inputs are the seeded synthetic cubes of synth/ (DESIGN.md §4), resident in HBM; each call is
+timed with CUDA events on the launching stream after 3 warm-ups, median of 10 (a 512 MB L2 flush
+between calls).  Prints one JSON object per config; the headline line is bench.py's (config 3).
+"""
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+import paper_2501_13664_b200 as d3  # noqa: E402
+
+CFG = {
+    1: ("drt", 0x001), 2: ("drt", 0xFFF), 3: ("drt", 0xFFF), 4: ("djt", 0x001), 5: ("drt", 0xFFF),
+}
+
+
+def run(cfg, iters=10):
+    kind, mask = CFG[cfg]
+    cube = torch.from_numpy(synth.config_input(cfg)).cuda()
+    B, N = cube.shape[0], cube.shape[1]
+    K = bin(mask).count("1")
+    fn = (lambda: d3.planes(cube, mask, out=out, workspace=ws)) if kind == "drt" else \
+        (lambda: d3.lines(cube, mask, out=out, workspace=ws))
+    o = d3.make_opts(batch=B, in_dtype=d3._dtype_code(cube), out_dtype=d3.DRT3D_F32 if cube.dtype == torch.float32
+                     else d3.DRT3D_I32)
+    if kind == "drt":
+        out = torch.empty((B, K, N, N, 3 * N), dtype=torch.float32 if cube.dtype == torch.float32 else torch.int32,
+                          device="cuda")
+        wsb = d3.drt3d_planes_workspace_size(N, mask, o)
+    else:
+        out = torch.empty((B, K, N, N, 2 * N, 2 * N), dtype=torch.float32 if cube.dtype == torch.float32 else torch.int32,
+                          device="cuda")
+        wsb = d3.djt3d_lines_workspace_size(N, mask, o)
+    ws = torch.empty(max(wsb, 256), dtype=torch.uint8, device="cuda")
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(iters):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ms = statistics.median(ts)
+    vox = B * N ** 3
+    cells = out.numel()
+    res = {"config": cfg, "transform": kind, "N": N, "batch": B, "dodecants": K, "dtype": str(cube.dtype),
+           "ms_median": ms, "ms_best": min(ts), "gvoxel_per_s": vox / (ms * 1e-3) / 1e9,
+           "out_cells_per_s": cells / (ms * 1e-3), "out_bytes": out.numel() * out.element_size(),
+           "out_write_gbs": out.numel() * out.element_size() / (ms * 1e-3) / 1e9}
+    if kind == "drt":
+        res["gplanes_per_s"] = B * K * N * N * (2 * N - 1) / (ms * 1e-3) / 1e9
+    return res
+
+
+if __name__ == "__main__":
+    cfgs = [int(a) for a in sys.argv[1:]] or [1, 2, 3, 4, 5]
+    for c in cfgs:
+        print(json.dumps(run(c, iters=10 if len(sys.argv) == 1 else 2)), flush=True)

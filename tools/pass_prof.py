@@ -12,7 +12,7 @@ for _ in range(3):
 torch.cuda.synchronize()
 buf = (ctypes.c_ulonglong * 16)()
 L.d3_pass_prof_read(buf)
-out = d3.planes(cube, 0x001)
+out = d3.planes(cube, 0xFFF)
 torch.cuda.synchronize()
 L.d3_pass_prof_read(buf)
 v = list(buf)

@@ -11,7 +11,7 @@ for _ in range(3):
     out = d3.planes(cube, 0xFFF)
 torch.cuda.synchronize()
 buf = (ctypes.c_ulonglong * 16)()
-for mask, name in ((0x001, "dodecant 0 (z-fast)"), (0x010, "dodecant 4 (y-fast)"), (0x100, "dodecant 8 (x-fast)")):
+for mask, name in ((0xFFF, "all 12 dodecants (one launch)"), (0x001, "dodecant 0 (z-fast)"), (0x010, "dodecant 4 (y-fast)"), (0x100, "dodecant 8 (x-fast)")):
     L.d3_swar_prof_read(buf)
     out = d3.planes(cube, mask)
     torch.cuda.synchronize()
