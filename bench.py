@@ -261,9 +261,12 @@ def run_ours(args):
     peak, peak_kind = _peaks()
     # algorithmic bytes: whole call = cube read once + output written once
     call_bytes = N ** 3 * 1 + K_DOD * N * N * 3 * N * 4
-    # dominant kernel = final pass, one launch per dodecant: reads the stage-4
-    # partial transform on its support (N^2 rows x (N+30) u16), writes N^2 x 3N int32
-    final_bytes = N * N * (N + 30) * 2 + N * N * 3 * N * 4
+    # dominant kernel = final pass; per dodecant it reads the stage-4 partial transform on its
+    # support (N^2 rows x (N+30) u16) and writes N^2 x 3N int32.  One launch covers all the
+    # dodecants of a chunk (12 at N=256: DESIGN.md §5), so the bytes per launch scale with that.
+    final_launches_per_step = max(1, len(kind_ms[2]) // max(1, args.steps))
+    dod_per_final_launch = K_DOD / final_launches_per_step
+    final_bytes = int(dod_per_final_launch * (N * N * (N + 30) * 2 + N * N * 3 * N * 4))
     fin_ms = statistics.mean(kind_ms[2]) if kind_ms[2] else float("nan")
     first_ms = statistics.mean(kind_ms[0]) if kind_ms[0] else float("nan")
     achieved = final_bytes / (fin_ms * 1e-3) / 1e9
@@ -328,7 +331,7 @@ def run_ours(args):
             "roofline": {"kernel": "drt_pass_kernel<K=4> final pass", "bound": "hbm", "achieved": achieved,
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "traffic_source": traffic_src,
-                         "algorithmic_bytes_per_launch": final_bytes,
+                         "algorithmic_bytes_per_launch": final_bytes, "dodecants_per_launch": dod_per_final_launch,
                          "launch_ms": fin_ms, "first_pass_ms": first_ms, "share_of_step": share},
             "gpu_launches": launches,
             "clocks": clocks,

@@ -299,6 +299,9 @@ drt_first_swar_kernel(const DrtPass p) {
     // tile elements [0, rho) (its head belongs to the previous tile).
     uint16_t *outp = reinterpret_cast<uint16_t *>(p.out);
     const long long out_inst = (long long)li * p.out_inst_stride;
+#ifdef D3_STAGE_EVICT_LAST
+    const uint64_t keep_pol = l2_evict_last();
+#endif
     const int mK = (1 << p.next_k) - 1;
     const int wv1 = V1 & mK, wv2 = V2 & mK;
     constexpr int NCK = T / 8;
@@ -319,7 +322,11 @@ drt_first_swar_kernel(const DrtPass p) {
             for (int i = 0; i < 4; ++i) v[i] = __byte_perm(w[4 * k + i], w[4 * k + i + 1], sel);
             if (d0 + 8 * k < p.out_width) {
                 if (k == NCK - 1) store_chunk_head<2>(dst + 8 * k, v, 8 - rho);
+#ifdef D3_STAGE_EVICT_LAST
+                else st_hint_v4(dst + 8 * k, v[0], v[1], v[2], v[3], keep_pol);
+#else
                 else *reinterpret_cast<uint4 *>(dst + 8 * k) = make_uint4(v[0], v[1], v[2], v[3]);
+#endif
             }
         }
         if (rho > 0 && d0 >= 8) {

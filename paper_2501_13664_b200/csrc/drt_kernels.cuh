@@ -340,6 +340,48 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
                     put4(fx ? wf * S + other : other * S + wf, gq, make_uint4(q4[0], q4[1], q4[2], q4[3]));
                 }
             }
+        } else if (sizeof(In) == 4 && K >= 2 && p.vec_ok && (z0 & 3) == 0 && (o.fast != 2 || o.sz > 0)) {
+            // 32-bit voxels: LDG.128 = 4 voxels.  Along z' (forward) they are one staged chunk;
+            // along x' or y' they are 4 rows at one z', so 4 consecutive z' are loaded per item
+            // and transposed in registers (reversed axes: the 4 values in reverse order).
+            constexpr int NQ4 = BW / 4;
+            if (o.fast == 2) {
+                for (int it = tid; it < S * S * NQ4; it += blockDim.x) {
+                    const int slot = it / NQ4, q = it - slot * NQ4;
+                    const int w1 = slot / S, w2 = slot - w1 * S, z = z0 + 4 * q;
+                    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+                    if ((unsigned)z < (unsigned)N)
+                        v = __ldg(reinterpret_cast<const uint4 *>(cube + o.off0 + (long long)(xb + w1) * o.sx +
+                                                                  (long long)(yb + w2) * o.sy + z));
+                    put4(slot, q, v);
+                }
+            } else {
+                const bool fy = o.fast == 1;
+                const long long sf = fy ? o.sy : o.sx, so = fy ? o.sx : o.sy;
+                const int fb = fy ? yb : xb, ob = fy ? xb : yb;
+                for (int it = tid; it < S * (S / 4) * NQ4; it += blockDim.x) {
+                    const int q = it % NQ4, rest = it / NQ4, g4 = rest % (S / 4), other = rest / (S / 4);
+                    uint32_t v[4][4];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const int z = z0 + 4 * q + t;
+                        uint4 a = make_uint4(0u, 0u, 0u, 0u);
+                        if ((unsigned)z < (unsigned)N) {
+                            const long long b = o.off0 + (long long)(ob + other) * so + (long long)z * o.sz +
+                                                (sf > 0 ? (long long)(fb + 4 * g4) : -(long long)(fb + 4 * g4 + 3));
+                            a = __ldg(reinterpret_cast<const uint4 *>(cube + b));
+                        }
+                        const uint32_t av[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) v[t][j] = av[sf > 0 ? j : 3 - j];
+                    }
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int f = 4 * g4 + j;
+                        put4(fy ? other * S + f : f * S + other, q, make_uint4(v[0][j], v[1][j], v[2][j], v[3][j]));
+                    }
+                }
+            }
         } else {
             // generic (any voxel type, any orientation, small N): element by element
             for (int i = tid; i < S * S * BW; i += blockDim.x) {
@@ -533,10 +575,19 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
             __syncthreads();
             if (tid == 0) {
                 const uint32_t src = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+#ifdef D3_TMA_EVICT_FIRST
+                uint64_t pol;
+                asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+                asm volatile(
+                    "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2, %3, %4}], [%5], %6;" ::"l"(&omap),
+                    "r"(d0), "r"(sg2 << K), "r"(sg1 << K), "r"(inst), "r"(src), "l"(pol)
+                    : "memory");
+#else
                 asm volatile(
                     "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(&omap),
                     "r"(d0), "r"(sg2 << K), "r"(sg1 << K), "r"(inst), "r"(src)
                     : "memory");
+#endif
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             }
