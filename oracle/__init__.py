@@ -249,3 +249,43 @@ def djt_lines(cube: np.ndarray, mask: int = 0x001, table: int = tables.TABLE_HEM
     ks = [k for k in range(12) if (mask >> k) & 1]
     out = np.stack([np.stack([djt_alg3(orient(c[b], rows[k])) for k in ks]) for b in range(c.shape[0])])
     return out[0] if single else out
+
+
+# ------------------------------------------------- adjoints (F-1) ----
+
+def unorient(h: np.ndarray, row) -> np.ndarray:
+    """Transpose of `orient` (a voxel permutation, so its inverse): undo the flips
+    of reading A, then the axis permutation."""
+    g = np.asarray(h)
+    for j, p in enumerate(row):
+        if p < 0:
+            g = np.flip(g, axis=j)
+    perm = [abs(p) - 1 for p in row]
+    inv = [perm.index(a) for a in range(3)]
+    return np.ascontiguousarray(np.transpose(g, inv))
+
+
+def drt_planes_adjoint(coef: np.ndarray, mask: int = 0xFFF, table: int = tables.TABLE_HEMISPHERE) -> np.ndarray:
+    """Backprojection of the stacked DRT coefficients [B][K][N][N][3N] (or [K][N][N][3N]):
+    sum over the dodecants k of unorient_k(adjoint of Alg. 1), fp64."""
+    c = np.asarray(coef)
+    single = c.ndim == 4
+    if single:
+        c = c[None]
+    rows = tables.table(table, "drt")
+    ks = [k for k in range(12) if (mask >> k) & 1]
+    out = np.stack([sum(unorient(drt_adjoint(c[b][j]), rows[k]) for j, k in enumerate(ks)) for b in range(c.shape[0])])
+    return out[0] if single else out
+
+
+def djt_lines_adjoint(coef: np.ndarray, mask: int = 0x001, table: int = tables.TABLE_HEMISPHERE) -> np.ndarray:
+    """Backprojection of stacked DJT coefficients [B][K][N][N][2N][2N] (or [K]...):
+    sum over the dodecants of unorient_k(adjoint of Alg. 3), fp64."""
+    c = np.asarray(coef)
+    single = c.ndim == 5
+    if single:
+        c = c[None]
+    rows = tables.table(table, "djt")
+    ks = [k for k in range(12) if (mask >> k) & 1]
+    out = np.stack([sum(unorient(djt_adjoint(c[b][j]), rows[k]) for j, k in enumerate(ks)) for b in range(c.shape[0])])
+    return out[0] if single else out
