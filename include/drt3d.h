@@ -114,6 +114,29 @@ drt3d_status djt3d_lines(const void *cube, int N, uint32_t dodecant_mask, void *
                          const drt3d_opts *opts, void *workspace, size_t workspace_bytes,
                          void *stream);
 
+/* ------------------------------------------------------------- adjoints --
+ * Backprojection = the transpose of the transforms above:
+ * eq:invmap3Dsummation / eq:invmap3DJsummation
+ * run in reversed stage order, then the
+ * transposes of the seeding step and of the dodecant orientation.
+ *   cube(c) = sum_{k in mask} sum_{s1,s2,D} coef_k(s1,s2,D) [c on plane (s1,s2,D) of k]
+ * (lines likewise), i.e. <A f, coef> = <f, A^T coef> for every f.
+ * coef: the stacked output layout of the forward call ([batch][K][N][N][3N] for
+ * planes, [batch][K][N][N][2N][2N] for lines) with element type opts->out_dtype
+ * (I32: exact sums mod 2^32; F32: fp32 accumulation); cube: [batch][N][N][N]
+ * of the same element type (opts->in_dtype is ignored).  STACKED layout only.
+ * Workspace: two stage buffers (query the size).                              */
+drt3d_status drt3d_planes_adjoint_workspace_size(int N, uint32_t dodecant_mask, const drt3d_opts *opts,
+                                                 size_t *bytes);
+drt3d_status drt3d_planes_adjoint(const void *coef, int N, uint32_t dodecant_mask, void *cube,
+                                  const drt3d_opts *opts, void *workspace, size_t workspace_bytes,
+                                  void *stream);
+drt3d_status djt3d_lines_adjoint_workspace_size(int N, uint32_t dodecant_mask, const drt3d_opts *opts,
+                                                size_t *bytes);
+drt3d_status djt3d_lines_adjoint(const void *coef, int N, uint32_t dodecant_mask, void *cube,
+                                 const drt3d_opts *opts, void *workspace, size_t workspace_bytes,
+                                 void *stream);
+
 /* --------------------------------------------------------- host buffers --
  * End-to-end variants: `host_cube` and `host_out` are HOST pointers (pinned
  * for full speed); `dev_cube` (>= cube bytes), `dev_out` (>= out bytes) and

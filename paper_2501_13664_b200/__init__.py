@@ -25,7 +25,9 @@ DRT3D_TABLE_HEMISPHERE, DRT3D_TABLE_PRINTED, DRT3D_TABLE_SHARED = range(3)
 # names declared in include/drt3d.h
 C_FUNCTIONS = ("drt3d_status_string", "drt3d_orientation_table", "drt3d_planes_out_elems",
                "drt3d_planes_workspace_size", "drt3d_planes", "djt3d_lines_out_elems",
-               "djt3d_lines_workspace_size", "djt3d_lines", "drt3d_planes_host", "djt3d_lines_host")
+               "djt3d_lines_workspace_size", "djt3d_lines", "drt3d_planes_host", "djt3d_lines_host",
+               "drt3d_planes_adjoint_workspace_size", "drt3d_planes_adjoint",
+               "djt3d_lines_adjoint_workspace_size", "djt3d_lines_adjoint")
 
 
 class Drt3dError(RuntimeError):
@@ -70,6 +72,12 @@ def lib() -> ctypes.CDLL:
         f = getattr(L, t + "_host")
         f.restype = i32
         f.argtypes = [vp, i32, u32, vp, po, vp, vp, vp, sz, vp]
+        f = getattr(L, t + "_adjoint_workspace_size")
+        f.restype = i32
+        f.argtypes = [i32, u32, po, ctypes.POINTER(sz)]
+        f = getattr(L, t + "_adjoint")
+        f.restype = i32
+        f.argtypes = [vp, i32, u32, vp, po, vp, sz, vp]
     _lib = L
     return L
 
@@ -203,3 +211,47 @@ def lines(cube, mask: int = 0x001, table: int = DRT3D_TABLE_HEMISPHERE, out=None
                     workspace.data_ptr() if workspace is not None else None, ws_bytes, st)
     _check(s, "djt3d_lines")
     return out if cube.dim() == 4 else out[0]
+
+
+# ------------------------------------------------------------ adjoints (F-1)
+
+def _adjoint(kind, coef, mask, table, cube, workspace, stream, opts):
+    import torch
+    if not coef.is_cuda:
+        raise Drt3dError("coef must be a CUDA tensor")
+    c = coef.contiguous()
+    nd = 5 if kind == "drt" else 6
+    if c.dim() == nd - 1:
+        c = c.unsqueeze(0)
+    if c.dim() != nd:
+        raise Drt3dError("coef must be the stacked forward layout")
+    B, N = c.shape[0], c.shape[2]
+    dt = {torch.int32: DRT3D_I32, torch.float32: DRT3D_F32}[c.dtype]
+    o = make_opts(batch=B, in_dtype=dt, out_dtype=dt, table=table)
+    if opts is not None:
+        o.events, o.max_events, o.launches, o.launch_kind = opts.events, opts.max_events, opts.launches, opts.launch_kind
+    if cube is None:
+        cube = torch.empty((B, N, N, N), dtype=c.dtype, device=c.device)
+    L = lib()
+    b = ctypes.c_size_t(0)
+    _check(getattr(L, f"{'drt3d_planes' if kind == 'drt' else 'djt3d_lines'}_adjoint_workspace_size")(
+        N, mask, ctypes.byref(o), ctypes.byref(b)), "adjoint_workspace_size")
+    if workspace is None:
+        workspace = torch.empty(max(b.value, 256), dtype=torch.uint8, device=c.device)
+    st = stream if stream is not None else torch.cuda.current_stream(c.device).cuda_stream
+    fn = L.drt3d_planes_adjoint if kind == "drt" else L.djt3d_lines_adjoint
+    _check(fn(c.data_ptr(), N, mask, cube.data_ptr(), ctypes.byref(o), workspace.data_ptr(), b.value, st),
+           f"{kind} adjoint")
+    return cube if coef.dim() == nd else cube[0]
+
+
+def planes_adjoint(coef, mask: int = 0xFFF, table: int = DRT3D_TABLE_HEMISPHERE, cube=None, workspace=None,
+                   stream=None, opts: drt3d_opts | None = None):
+    """Backprojection of stacked DRT coefficients [B,K,N,N,3N] (int32 / float32) -> [B,N,N,N]."""
+    return _adjoint("drt", coef, mask, table, cube, workspace, stream, opts)
+
+
+def lines_adjoint(coef, mask: int = 0x001, table: int = DRT3D_TABLE_HEMISPHERE, cube=None, workspace=None,
+                  stream=None, opts: drt3d_opts | None = None):
+    """Backprojection of stacked DJT coefficients [B,K,N,N,2N,2N] (int32 / float32) -> [B,N,N,N]."""
+    return _adjoint("djt", coef, mask, table, cube, workspace, stream, opts)

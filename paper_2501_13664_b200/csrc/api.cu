@@ -7,6 +7,7 @@
 #include <cstring>
 
 #include "dispatch.h"
+#include "adjoint.h"
 
 using namespace d3;
 
@@ -560,6 +561,60 @@ drt3d_status djt3d_lines(const void *cube, int N, uint32_t mask, void *out, cons
     s = check_ptrs(cube, out, workspace, workspace_bytes, P, o, 1);
     if (s != DRT3D_OK) return s;
     return run_djt(cube, mask, out, o, P, workspace, reinterpret_cast<cudaStream_t>(stream));
+}
+
+// ---------------------------------------------------------------- adjoints
+static drt3d_status adjoint_check(int transform, int N, uint32_t mask, const drt3d_opts &o, int &n) {
+    n = ilog2_exact(N);
+    if (n < 0 || mask == 0 || mask >= (1u << 12) || o.batch < 1) return DRT3D_ERR_INVALID_ARG;
+    if (o.out_dtype != DRT3D_I32 && o.out_dtype != DRT3D_F32) return DRT3D_ERR_INVALID_ARG;
+    if (o.table < 0 || o.table > 2 || o.layout != DRT3D_LAYOUT_STACKED) return DRT3D_ERR_INVALID_ARG;
+    (void)transform;
+    return DRT3D_OK;
+}
+
+static drt3d_status adjoint_ws(int transform, int N, uint32_t mask, const drt3d_opts *opts, size_t *bytes) {
+    if (!bytes) return DRT3D_ERR_INVALID_ARG;
+    drt3d_opts tmp;
+    const drt3d_opts &o = opts_or_default(opts, tmp);
+    int n;
+    drt3d_status s = adjoint_check(transform, N, mask, o, n);
+    if (s != DRT3D_OK) return s;
+    *bytes = d3::adjoint_workspace_bytes(transform, N);
+    return DRT3D_OK;
+}
+
+static drt3d_status adjoint_run(int transform, const void *coef, int N, uint32_t mask, void *cube,
+                                const drt3d_opts *opts, void *ws, size_t ws_bytes, void *stream) {
+    drt3d_opts tmp;
+    const drt3d_opts &o = opts_or_default(opts, tmp);
+    int n;
+    drt3d_status s = adjoint_check(transform, N, mask, o, n);
+    if (s != DRT3D_OK) return s;
+    if (!coef || !cube) return DRT3D_ERR_INVALID_ARG;
+    if (!ws || ws_bytes < d3::adjoint_workspace_bytes(transform, N)) return DRT3D_ERR_WORKSPACE;
+    const int K = popcount12(mask);
+    const size_t cb = (size_t)o.batch * N * N * N * 4;
+    const size_t ob = (size_t)o.batch * K * N * N * (transform == 0 ? 3 * N : 4 * N * N) * 4;
+    const uintptr_t c0 = reinterpret_cast<uintptr_t>(cube), o0 = reinterpret_cast<uintptr_t>(coef);
+    if (c0 < o0 + ob && o0 < c0 + cb) return DRT3D_ERR_INVALID_ARG;   // overlap
+    return d3::run_adjoint(transform, coef, N, n, table_rows(o.table, transform), mask, o.batch, o.out_dtype, cube, ws,
+                           reinterpret_cast<cudaStream_t>(stream), o.launches);
+}
+
+drt3d_status drt3d_planes_adjoint_workspace_size(int N, uint32_t mask, const drt3d_opts *opts, size_t *bytes) {
+    return adjoint_ws(0, N, mask, opts, bytes);
+}
+drt3d_status drt3d_planes_adjoint(const void *coef, int N, uint32_t mask, void *cube, const drt3d_opts *opts,
+                                  void *ws, size_t ws_bytes, void *stream) {
+    return adjoint_run(0, coef, N, mask, cube, opts, ws, ws_bytes, stream);
+}
+drt3d_status djt3d_lines_adjoint_workspace_size(int N, uint32_t mask, const drt3d_opts *opts, size_t *bytes) {
+    return adjoint_ws(1, N, mask, opts, bytes);
+}
+drt3d_status djt3d_lines_adjoint(const void *coef, int N, uint32_t mask, void *cube, const drt3d_opts *opts,
+                                 void *ws, size_t ws_bytes, void *stream) {
+    return adjoint_run(1, coef, N, mask, cube, opts, ws, ws_bytes, stream);
 }
 
 static drt3d_status host_variant(int transform, const void *host_cube, int N, uint32_t mask, void *host_out,
