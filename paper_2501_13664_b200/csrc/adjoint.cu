@@ -64,6 +64,8 @@ __global__ void drt_adj_scatter(const T *__restrict__ b0, T *__restrict__ cube, 
 //   b^m(i, d1, d2) = sum_{b1,b2} b^{m+1}(v + 2^(n-m-1) b1 + 2^(n-m) sg1 + 2^n b2 + 2^(n+1) sg2,
 //                                        d1 - vm (b1 + sg1), d2 - vm (b2 + sg2)).
 // Stage n-1 reads the caller's [s1][s2][D1][D2] layout (inverse of separateS1S2: row s1 + N s2).
+// Only the first 2^(n+m) rows of a stage-m buffer exist (m slope bits per axis), so a stage
+// computes exactly those.
 template <class T>
 __global__ void djt_adj_stage(const T *__restrict__ in, T *__restrict__ out, int N, int n, int m, bool from_coef,
                               long long ncell) {
@@ -128,7 +130,10 @@ static drt3d_status run_adj(int transform, const void *coef, int N, int n, const
             for (int m = n - 1; m >= 0; --m) {
                 const T *in = (m == n - 1) ? src : buf[cur ^ 1];
                 if (transform == 0) drt_adj_stage<T><<<nblk(cells), kThreads, 0, st>>>(in, buf[cur], N, m, cells);
-                else djt_adj_stage<T><<<nblk(cells), kThreads, 0, st>>>(in, buf[cur], N, n, m, m == n - 1, cells);
+                else {
+                    const long long rows_m = 1LL << (n + m), ncell = rows_m * W * W;
+                    djt_adj_stage<T><<<nblk(ncell), kThreads, 0, st>>>(in, buf[cur], N, n, m, m == n - 1, ncell);
+                }
                 ++nl;
                 cur ^= 1;
             }

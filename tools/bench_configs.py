@@ -65,7 +65,38 @@ def run(cfg, iters=10):
     return res
 
 
+def run_adjoint(cfg, iters=5):
+    """Backprojection (F-1) on the coefficient shape of config cfg (3: DRT N=256 x12, 4: DJT N=64)."""
+    kind, mask = CFG[cfg]
+    N = {3: 256, 4: 64}[cfg]
+    K = bin(mask).count("1")
+    shape = (1, K, N, N, 3 * N) if kind == "drt" else (1, K, N, N, 2 * N, 2 * N)
+    g = torch.Generator(device="cuda").manual_seed(cfg)
+    coef = torch.randint(0, 1000, shape, dtype=torch.int32, device="cuda", generator=g)
+    cube = torch.empty((1, N, N, N), dtype=torch.int32, device="cuda")
+    fn = (lambda: d3.planes_adjoint(coef, mask, cube=cube)) if kind == "drt" else \
+        (lambda: d3.lines_adjoint(coef, mask, cube=cube))
+    for _ in range(2):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(iters):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ms = statistics.median(ts)
+    return {"config": f"adjoint-{cfg}", "transform": kind + "_adjoint", "N": N, "batch": 1, "dodecants": K,
+            "ms_median": ms, "gvoxel_per_s": N ** 3 / (ms * 1e-3) / 1e9,
+            "coef_read_gbs": coef.numel() * 4 / (ms * 1e-3) / 1e9}
+
+
 if __name__ == "__main__":
     cfgs = [int(a) for a in sys.argv[1:]] or [1, 2, 3, 4, 5]
     for c in cfgs:
         print(json.dumps(run(c, iters=10 if len(sys.argv) == 1 else 2)), flush=True)
+    if len(sys.argv) == 1:
+        for c in (3, 4):
+            print(json.dumps(run_adjoint(c)), flush=True)
