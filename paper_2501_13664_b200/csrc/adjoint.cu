@@ -5,12 +5,14 @@
 // the dodecant orientation (a scatter back into the original cube, accumulated over dodecants
 // in a fixed order, so results are deterministic).
 //
-// First version: one thread per output cell and stage, gathers straight from HBM/L2 (no
-// shared-memory blocking).  Integer lanes wrap mod 2^32 like the forward transform; float lanes
-// accumulate in fp32 in the oracle's order (b1 outer, b2 inner).
+// One thread per output cell; a launch applies L consecutive gather stages at once (their
+// composition: 4^L reads per cell for both transforms), straight from
+// HBM/L2 with no shared-memory blocking.  Integer lanes wrap mod 2^32 like the forward transform;
+// float lanes accumulate in fp32.
 #include "drt3d.h"
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "adjoint.h"
 
@@ -18,45 +20,221 @@ namespace d3 {
 
 template <class T> __device__ __forceinline__ T zero_v() { return T(0); }
 
-// ---- DRT stage m (b^{m+1} -> b^m), rows ii = sg1 + 2^m v1m + 2^(m+1) v1 (same for jj), D in [0, 3N):
+// ---- DRT: L consecutive stages m_lo..m_lo+L-1 in one launch (b^{m_lo+L} -> b^{m_lo}).
+// Stage m (b^{m+1} -> b^m), rows ii = sg1 + 2^m v1m + 2^(m+1) v1 (same for jj), D in [0, 3N):
 //   b^m(ii, jj, d) = sum_{b1, b2} b^{m+1}(b1 + 2 sg1 + 2^(m+1) v1, b2 + 2 sg2 + 2^(m+1) v2,
 //                                      d - v1m (b1 + sg1) - v2m (b2 + sg2)),  reads below 0 are 0.
-template <class T>
-__global__ void drt_adj_stage(const T *__restrict__ in, T *__restrict__ out, int N, int m, long long ncell) {
-    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= ncell) return;
-    const int W = 3 * N;
-    const int d = (int)(idx % W);
-    const long long row = idx / W;
-    const int jj = (int)(row % N), ii = (int)(row / N);
-    const int msk = (1 << m) - 1;
-    const int sg1 = ii & msk, v1m = (ii >> m) & 1, v1 = ii >> (m + 1);
-    const int sg2 = jj & msk, v2m = (jj >> m) & 1, v2 = jj >> (m + 1);
-    T acc = zero_v<T>();
+// The maps act on the two row axes separately and all shifts are >= 0, so L stages compose into
+// 2^L (row, shift) pairs per axis; a composite term whose final index is >= 0 had every
+// intermediate index >= 0 too, hence the composition is exact (only the fp32 summation order
+// differs from the stage-by-stage oracle).
+template <int L>
+__device__ __forceinline__ void drt_axis_terms(int ii, int m_lo, int (&row)[1 << L], int (&sh)[1 << L]) {
+    row[0] = ii;
+    sh[0] = 0;
 #pragma unroll
-    for (int b1 = 0; b1 < 2; ++b1)
+    for (int l = 0; l < L; ++l) {
+        const int m = m_lo + l, cnt = 1 << l;
 #pragma unroll
-        for (int b2 = 0; b2 < 2; ++b2) {
-            const int dd = d - v1m * (b1 + sg1) - v2m * (b2 + sg2);
-            if (dd < 0) continue;
-            const int oi = b1 + (sg1 << 1) + (v1 << (m + 1)), oj = b2 + (sg2 << 1) + (v2 << (m + 1));
-            acc = acc + in[((long long)oi * N + oj) * W + dd];
+        for (int t = cnt - 1; t >= 0; --t) {
+            const int r = row[t], s = sh[t];
+            const int sg = r & ((1 << m) - 1), vm = (r >> m) & 1, v = r >> (m + 1);
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {
+                row[2 * t + b] = b + (sg << 1) + (v << (m + 1));
+                sh[2 * t + b] = s + vm * (b + sg);
+            }
         }
-    out[idx] = acc;
+    }
+}
+
+// grid: x = output row ii * N + jj; the block's threads stride along D, so the row's terms are
+// set up once per thread rather than once per cell
+template <class T, int L>
+__global__ void drt_adj_stage(const T *__restrict__ in, T *__restrict__ out, int N, int m_lo) {
+    const int W = 3 * N;
+    const int ii = blockIdx.x / N, jj = blockIdx.x - ii * N;
+    int r1[1 << L], s1[1 << L], r2[1 << L], s2[1 << L];
+    drt_axis_terms<L>(ii, m_lo, r1, s1);
+    drt_axis_terms<L>(jj, m_lo, r2, s2);
+    constexpr int NT = 1 << (2 * L);
+    // per-term base pointers pre-offset by the term's shift: term t of cell d reads p[t][d]
+    // when d >= sh[t] (never dereferenced otherwise)
+    const T *p[NT];
+    int sh[NT];
+#pragma unroll
+    for (int a = 0; a < (1 << L); ++a)
+#pragma unroll
+        for (int b = 0; b < (1 << L); ++b) {
+            const int t = a * (1 << L) + b;
+            sh[t] = s1[a] + s2[b];
+            p[t] = in + ((long long)(r1[a] * N + r2[b]) * W - sh[t]);
+        }
+    // walk the term pointers along D (kept in registers: the empty asm stops the compiler from
+    // rebuilding each address from the kernel parameter per load)
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+        p[t] += threadIdx.x;
+        asm volatile("" : "+l"(p[t]));
+    }
+    T *dst = out + (size_t)blockIdx.x * W + threadIdx.x;
+    for (int d = threadIdx.x; d < W; d += blockDim.x) {
+        T acc = zero_v<T>();
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            if (d >= sh[t]) acc = acc + __ldg(p[t]);
+            p[t] += blockDim.x;
+        }
+        *dst = acc;
+        dst += blockDim.x;
+    }
+}
+
+// ---- DRT, shared-memory butterfly: the stage map sends the two output rows sg + 2^m vm + 2^(m+1) v
+// (vm = 0, 1) to the same two input rows 2 sg + b + 2^(m+1) v (b = 0, 1), per axis.  Groups of
+// 2^L rows per axis are therefore closed under L consecutive stages: a block loads its 4^L input
+// rows (level m_lo + L) into shared memory once, runs the L gather stages there (double-buffered,
+// whole rows of W = 3N cells, so every shifted read is in the buffer), and writes its 4^L output
+// rows (level m_lo).  HBM traffic per L stages: one read and one write of the stage buffer.
+// Tables (built by two threads per block): per level and axis the rows each slot holds, and per
+// stage, output row q and term k = 2 b1 + b2, the buffer offset (slot row * W - shift) and shift.
+template <int L>
+struct BflyTab {
+    int row[L + 1][2][1 << L];
+    int off[L][1 << (2 * L)][4];
+    int sh[L][1 << (2 * L)][4];
+};
+
+template <int L>
+__device__ void bfly_tables(BflyTab<L> &tab, int N, int W, int m_lo) {
+    constexpr int S = 1 << L;
+    __shared__ int src[L][2][S][2], shx[L][2][S][2];
+    if (threadIdx.x < 2) {
+        // group id per axis: the bits of the level-m_lo row other than m_lo .. m_lo+L-1
+        const int ng = N >> L, ax = threadIdx.x;
+        const int g = ax == 0 ? (int)blockIdx.x / ng : (int)blockIdx.x % ng;
+        const int lowm = (1 << m_lo) - 1;
+        for (int u = 0; u < S; ++u) tab.row[0][ax][u] = (g & lowm) | (u << m_lo) | ((g >> m_lo) << (m_lo + L));
+        for (int l = 0; l < L; ++l) {
+            const int m = m_lo + l;
+            int cnt = 0;
+            for (int u = 0; u < S; ++u) {
+                const int r = tab.row[l][ax][u];
+                const int sg = r & ((1 << m) - 1), vm = (r >> m) & 1, v = r >> (m + 1);
+                for (int b = 0; b < 2; ++b) {
+                    const int x = b + (sg << 1) + (v << (m + 1));
+                    int k = 0;
+                    while (k < cnt && tab.row[l + 1][ax][k] != x) ++k;
+                    if (k == cnt) tab.row[l + 1][ax][cnt++] = x;     // closure: cnt ends at exactly S
+                    src[l][ax][u][b] = k;
+                    shx[l][ax][u][b] = vm * (b + sg);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < L * S * S * 4; e += blockDim.x) {
+        const int k = e & 3, q = (e >> 2) % (S * S), l = (e >> 2) / (S * S);
+        const int u1 = q / S, u2 = q % S, b1 = k >> 1, b2 = k & 1;
+        const int sh = shx[l][0][u1][b1] + shx[l][1][u2][b2];
+        tab.sh[l][q][k] = sh;
+        tab.off[l][q][k] = (src[l][0][u1][b1] * S + src[l][1][u2][b2]) * W - sh;
+    }
+    __syncthreads();
+}
+
+// One buffer of 4^L whole rows; a stage computes every output this thread owns (rows q, columns
+// d = tid + 256 c, c < NC) into registers, then all threads write back after a barrier.
+template <class T, int L, int NC>
+__global__ void __launch_bounds__(256) drt_adj_bfly(const T *__restrict__ in, T *__restrict__ out, int N, int m_lo) {
+    extern __shared__ __align__(16) unsigned char adj_smem[];
+    constexpr int S = 1 << L, R = S * S;
+    const int W = 3 * N;
+    T *buf = reinterpret_cast<T *>(adj_smem);
+    __shared__ BflyTab<L> tab;
+    bfly_tables<L>(tab, N, W, m_lo);
+    const int tid = threadIdx.x;
+    // load the level-(m_lo + L) rows: 16-byte cp.async when rows are 16-byte multiples
+    const bool vec = (W % 4) == 0;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+        const T *g = in + ((size_t)tab.row[L][0][q / S] * N + tab.row[L][1][q % S]) * W;
+        T *dst = buf + q * W;
+        if (vec) {
+            for (int d = tid * 4; d < W; d += 1024) {
+                const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + d);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g + d) : "memory");
+            }
+        } else {
+            for (int d = tid; d < W; d += 256) dst[d] = __ldg(g + d);
+        }
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+    // stages m_lo + L - 1 .. m_lo (the adjoint runs them in decreasing m)
+    for (int l = L - 1; l >= 0; --l) {
+        T acc[R][NC];
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            int off[4], sh[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                off[k] = tab.off[l][q][k];
+                sh[k] = tab.sh[l][q][k];
+            }
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                const int d = tid + 256 * c;
+                T a = zero_v<T>();
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (d < W && d >= sh[k]) a = a + buf[off[k] + d];
+                acc[q][c] = a;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                const int d = tid + 256 * c;
+                if (d < W) buf[q * W + d] = acc[q][c];
+            }
+        __syncthreads();
+    }
+    // store the level-m_lo rows
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+        T *g = out + ((size_t)tab.row[0][0][q / S] * N + tab.row[0][1][q % S]) * W;
+        const T *src = buf + q * W;
+        if (vec) {
+            for (int d = tid * 4; d < W; d += 1024)
+                *reinterpret_cast<uint4 *>(g + d) = *reinterpret_cast<const uint4 *>(src + d);
+        } else {
+            for (int d = tid; d < W; d += 256) g[d] = src[d];
+        }
+    }
 }
 
 // ---- seeding transpose + orientation transpose: cube[c] (+)= b^0(x', y', 2N + z') with
-// oriented x'_j = c_{|p_j|} or N - 1 - c_{|p_j|} (reading A)
+// oriented x'_j = c_{|p_j|} or N - 1 - c_{|p_j|} (reading A).
+// grid: x = c0 * N + c1, threads along c2.
+__device__ __forceinline__ int orient(const int (&c)[3], int p, int N) {
+    const int a = (p < 0 ? -p : p) - 1;
+    const int v = a == 0 ? c[0] : (a == 1 ? c[1] : c[2]);
+    return p > 0 ? v : N - 1 - v;
+}
+
 template <class T>
 __global__ void drt_adj_scatter(const T *__restrict__ b0, T *__restrict__ cube, int N, int p0, int p1, int p2,
                                 bool first) {
-    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long n3 = (long long)N * N * N;
-    if (idx >= n3) return;
-    const int c[3] = {(int)(idx / ((long long)N * N)), (int)((idx / N) % N), (int)(idx % N)};
-    auto o = [&](int p) { const int a = (p < 0 ? -p : p) - 1; return p > 0 ? c[a] : N - 1 - c[a]; };
-    const int x = o(p0), y = o(p1), z = o(p2);
-    const T v = b0[((long long)x * N + y) * (3 * N) + 2 * N + z];
+    const int c2 = blockIdx.y * blockDim.x + threadIdx.x;
+    if (c2 >= N) return;
+    const int c0 = blockIdx.x / N;
+    const int c[3] = {c0, (int)blockIdx.x - c0 * N, c2};
+    const int x = orient(c, p0, N), y = orient(c, p1, N), z = orient(c, p2, N);
+    const T v = b0[((size_t)x * N + y) * (3 * N) + 2 * N + z];
+    const size_t idx = (size_t)blockIdx.x * N + c2;
     cube[idx] = first ? v : cube[idx] + v;
 }
 
@@ -65,49 +243,138 @@ __global__ void drt_adj_scatter(const T *__restrict__ b0, T *__restrict__ cube, 
 //                                        d1 - vm (b1 + sg1), d2 - vm (b2 + sg2)).
 // Stage n-1 reads the caller's [s1][s2][D1][D2] layout (inverse of separateS1S2: row s1 + N s2).
 // Only the first 2^(n+m) rows of a stage-m buffer exist (m slope bits per axis), so a stage
-// computes exactly those.
-template <class T>
-__global__ void djt_adj_stage(const T *__restrict__ in, T *__restrict__ out, int N, int n, int m, bool from_coef,
-                              long long ncell) {
-    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= ncell) return;
+// computes exactly those.  L stages compose into 4^L (row, shift1, shift2) terms, exact for the
+// same reason as the DRT's.
+// grid: x = (output row i, block of kD1 consecutive d1); threads stride along d2.
+constexpr int kD1 = 8;
+template <class T, int L>
+__global__ void djt_adj_stage(const T *__restrict__ in, T *__restrict__ out, int N, int n, int m_lo,
+                              bool from_coef) {
     const int W = 2 * N;
-    const int d2 = (int)(idx % W);
-    const int d1 = (int)((idx / W) % W);
-    const int i = (int)(idx / ((long long)W * W));
-    const int vm = i & 1, v = (i >> 1) & ((1 << (n - m - 1)) - 1);
-    const int sg1 = (i >> (n - m)) & ((1 << m) - 1), sg2 = i >> n;
-    T acc = zero_v<T>();
+    const int nb = (W + kD1 - 1) / kD1;
+    const int i = blockIdx.x / nb, d1_0 = (blockIdx.x - i * nb) * kD1;
+    constexpr int NT = 1 << (2 * L);
+    int row[NT], e1[NT], e2[NT];
+    row[0] = i;
+    e1[0] = 0;
+    e2[0] = 0;
 #pragma unroll
-    for (int b1 = 0; b1 < 2; ++b1)
+    for (int l = 0; l < L; ++l) {
+        const int m = m_lo + l, cnt = 1 << (2 * l);
 #pragma unroll
-        for (int b2 = 0; b2 < 2; ++b2) {
-            const int e1 = d1 - vm * (b1 + sg1), e2 = d2 - vm * (b2 + sg2);
-            if (e1 < 0 || e2 < 0) continue;
-            int o = v + (b1 << (n - m - 1)) + (sg1 << (n - m)) + (b2 << n) + (sg2 << (n + 1));
-            if (from_coef) o = (o % N) * N + o / N;          // packed s1 + N s2 -> caller row s1 N + s2
-            acc = acc + in[((long long)o * W + e1) * W + e2];
+        for (int t = cnt - 1; t >= 0; --t) {
+            const int r = row[t], a1 = e1[t], a2 = e2[t];
+            const int vm = r & 1, v = (r >> 1) & ((1 << (n - m - 1)) - 1);
+            const int sg1 = (r >> (n - m)) & ((1 << m) - 1), sg2 = r >> n;
+#pragma unroll
+            for (int b1 = 0; b1 < 2; ++b1)
+#pragma unroll
+                for (int b2 = 0; b2 < 2; ++b2) {
+                    const int k = 4 * t + 2 * b1 + b2;
+                    row[k] = v + (b1 << (n - m - 1)) + (sg1 << (n - m)) + (b2 << n) + (sg2 << (n + 1));
+                    e1[k] = a1 + vm * (b1 + sg1);
+                    e2[k] = a2 + vm * (b2 + sg2);
+                }
         }
-    out[idx] = acc;
+    }
+#pragma unroll
+    for (int t = 0; t < NT; ++t)
+        if (from_coef) row[t] = (row[t] % N) * N + row[t] / N;   // packed s1 + N s2 -> caller row s1 N + s2
+    for (int d1 = d1_0; d1 < d1_0 + kD1 && d1 < W; ++d1) {
+        T *dst = out + ((size_t)i * W + d1) * W;
+        for (int d2 = threadIdx.x; d2 < W; d2 += blockDim.x) {
+            T acc = zero_v<T>();
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const int f1 = d1 - e1[t], f2 = d2 - e2[t];
+                if (f1 >= 0 && f2 >= 0) acc = acc + in[((size_t)row[t] * W + f1) * W + f2];
+            }
+            dst[d2] = acc;
+        }
+    }
 }
 
 template <class T>
 __global__ void djt_adj_scatter(const T *__restrict__ b0, T *__restrict__ cube, int N, int p0, int p1, int p2,
                                 bool first) {
-    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long n3 = (long long)N * N * N;
-    if (idx >= n3) return;
-    const int c[3] = {(int)(idx / ((long long)N * N)), (int)((idx / N) % N), (int)(idx % N)};
-    auto o = [&](int p) { const int a = (p < 0 ? -p : p) - 1; return p > 0 ? c[a] : N - 1 - c[a]; };
-    const int x = o(p0), y = o(p1), z = o(p2);
+    const int c2 = blockIdx.y * blockDim.x + threadIdx.x;
+    if (c2 >= N) return;
+    const int c0 = blockIdx.x / N;
+    const int c[3] = {c0, (int)blockIdx.x - c0 * N, c2};
+    const int x = orient(c, p0, N), y = orient(c, p1, N), z = orient(c, p2, N);
     const int W = 2 * N;
-    const T v = b0[((long long)x * W + N + y) * W + N + z];
+    const T v = b0[((size_t)x * W + N + y) * W + N + z];
+    const size_t idx = (size_t)blockIdx.x * N + c2;
     cube[idx] = first ? v : cube[idx] + v;
 }
 
 namespace {
-constexpr int kThreads = 256;
-inline unsigned nblk(long long n) { return (unsigned)((n + kThreads - 1) / kThreads); }
+// threads per block along the fast (D or z) axis: a multiple of 32, at most 256
+inline unsigned tpb(int w) { return (unsigned)(w >= 256 ? 256 : ((w + 31) / 32) * 32); }
+inline unsigned chunks(int w) { return (unsigned)((w + tpb(w) - 1) / tpb(w)); }
+// threads per DRT stage row: about 8 cells per thread (per-thread term setup is ~130 instructions)
+inline unsigned row_threads(int w) {
+    const char *e = getenv("D3_ADJ_EPT");
+    const int ept = e ? atoi(e) : 8;
+    const int t = ((w + ept - 1) / ept + 31) / 32 * 32;
+    return (unsigned)(t < 32 ? 32 : (t > 1024 ? 1024 : t));
+}
+
+// stages fused per launch (default 1; D3_ADJ_L in 1..3 for measurement: 2 and 3 were slower)
+int adj_fuse() {
+    static const int l = [] {
+        const char *e = getenv("D3_ADJ_L");
+        const int v = e ? atoi(e) : 1;
+        return v < 1 ? 1 : (v > 3 ? 3 : v);
+    }();
+    return l;
+}
+
+// butterfly launch: 4^L rows per block in one shared-memory buffer, NC columns per thread
+template <class T, int L, int NC>
+void drt_bfly_nc(const T *in, T *out, int N, int m_lo, cudaStream_t st) {
+    const size_t smem = (size_t)(1 << (2 * L)) * 3 * N * sizeof(T);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(drt_adj_bfly<T, L, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    drt_adj_bfly<T, L, NC><<<(unsigned)((N >> L) * (N >> L)), 256, smem, st>>>(in, out, N, m_lo);
+}
+
+template <class T, int L>
+void drt_bfly(const T *in, T *out, int N, int m_lo, cudaStream_t st) {
+    const int nc = (3 * N + 255) / 256;
+    if (nc <= 1) drt_bfly_nc<T, L, 1>(in, out, N, m_lo, st);
+    else if (nc <= 3) drt_bfly_nc<T, L, 3>(in, out, N, m_lo, st);
+    else if (nc <= 6) drt_bfly_nc<T, L, 6>(in, out, N, m_lo, st);
+    else drt_bfly_nc<T, 1, 12>(in, out, N, m_lo, st);              // N = 1024: radix 2 only
+}
+
+// butterfly radix per launch: 2 (16 rows) up to N = 512, else 1 (D3_ADJ_BFLY=0 selects the
+// plain gather kernels, for measurement)
+inline int bfly_max(int N) {
+    const char *e = getenv("D3_ADJ_BFLY");
+    const int cap = e ? atoi(e) : 2;
+    return cap <= 0 ? 0 : (cap == 1 || N > 512 ? 1 : 2);
+}
+
+template <class T>
+void drt_stage(int L, const T *in, T *out, int N, int m_lo, cudaStream_t st) {
+    const dim3 g((unsigned)(N * N)), b(row_threads(3 * N));
+    if (L == 1) drt_adj_stage<T, 1><<<g, b, 0, st>>>(in, out, N, m_lo);
+    else if (L == 2) drt_adj_stage<T, 2><<<g, b, 0, st>>>(in, out, N, m_lo);
+    else drt_adj_stage<T, 3><<<g, b, 0, st>>>(in, out, N, m_lo);
+}
+
+template <class T>
+void djt_stage(int L, const T *in, T *out, int N, int n, int m_lo, bool from_coef, cudaStream_t st) {
+    const long long rows = 1LL << (n + m_lo);                      // live rows of b^{m_lo}
+    const dim3 g((unsigned)(rows * ((2 * N + kD1 - 1) / kD1))), b(tpb(2 * N));
+    if (L == 1) djt_adj_stage<T, 1><<<g, b, 0, st>>>(in, out, N, n, m_lo, from_coef);
+    else if (L == 2) djt_adj_stage<T, 2><<<g, b, 0, st>>>(in, out, N, n, m_lo, from_coef);
+    else djt_adj_stage<T, 3><<<g, b, 0, st>>>(in, out, N, n, m_lo, from_coef);
+}
 }  // namespace
 
 template <class T>
@@ -120,6 +387,9 @@ static drt3d_status run_adj(int transform, const void *coef, int N, int n, const
     const T *cf = reinterpret_cast<const T *>(coef);
     T *cb = reinterpret_cast<T *>(cube);
     const long long n3 = (long long)N * N * N;
+    const int Lb = transform == 0 ? bfly_max(N) : 0;
+    const int Lmax = Lb > 0 ? Lb : adj_fuse();
+    const dim3 sg((unsigned)(N * N), chunks(N)), sb(tpb(N));
     int nl = 0;
     for (int b = 0; b < batch; ++b) {
         int j = 0;
@@ -127,23 +397,25 @@ static drt3d_status run_adj(int transform, const void *coef, int N, int n, const
             if (!((mask >> k) & 1)) continue;
             const T *src = cf + ((long long)b * K + j) * cells;
             int cur = 0;
-            for (int m = n - 1; m >= 0; --m) {
-                const T *in = (m == n - 1) ? src : buf[cur ^ 1];
-                if (transform == 0) drt_adj_stage<T><<<nblk(cells), kThreads, 0, st>>>(in, buf[cur], N, m, cells);
-                else {
-                    const long long rows_m = 1LL << (n + m), ncell = rows_m * W * W;
-                    djt_adj_stage<T><<<nblk(ncell), kThreads, 0, st>>>(in, buf[cur], N, n, m, m == n - 1, ncell);
-                }
+            for (int m_hi = n - 1; m_hi >= 0;) {
+                const int L = m_hi + 1 < Lmax ? m_hi + 1 : Lmax, m_lo = m_hi - L + 1;
+                const T *in = (m_hi == n - 1) ? src : buf[cur ^ 1];
+                if (transform == 0 && Lb > 0) {
+                    if (L == 2) drt_bfly<T, 2>(in, buf[cur], N, m_lo, st);
+                    else drt_bfly<T, 1>(in, buf[cur], N, m_lo, st);
+                } else if (transform == 0) drt_stage<T>(L, in, buf[cur], N, m_lo, st);
+                else djt_stage<T>(L, in, buf[cur], N, n, m_lo, m_hi == n - 1, st);
                 ++nl;
                 cur ^= 1;
+                m_hi = m_lo - 1;
             }
             const T *b0 = buf[cur ^ 1];
             if (transform == 0)
-                drt_adj_scatter<T><<<nblk(n3), kThreads, 0, st>>>(b0, cb + (long long)b * n3, N, rows[k][0], rows[k][1],
-                                                                  rows[k][2], j == 0);
+                drt_adj_scatter<T><<<sg, sb, 0, st>>>(b0, cb + (long long)b * n3, N, rows[k][0], rows[k][1],
+                                                      rows[k][2], j == 0);
             else
-                djt_adj_scatter<T><<<nblk(n3), kThreads, 0, st>>>(b0, cb + (long long)b * n3, N, rows[k][0], rows[k][1],
-                                                                  rows[k][2], j == 0);
+                djt_adj_scatter<T><<<sg, sb, 0, st>>>(b0, cb + (long long)b * n3, N, rows[k][0], rows[k][1],
+                                                      rows[k][2], j == 0);
             ++nl;
             ++j;
         }
