@@ -137,6 +137,34 @@ drt3d_status djt3d_lines_adjoint(const void *coef, int N, uint32_t dodecant_mask
                                  const drt3d_opts *opts, void *workspace, size_t workspace_bytes,
                                  void *stream);
 
+/* ---------------------------------------------------- iterative inverse --
+ * Iterative inverse of the 3D DRT: Press's
+ * iterative improvement x <- x + B (b - A x), x_0 = 0, where B is the multigrid
+ * approximate inverse built from the 3D high-pass filter h,
+ * the prolongation P and the restriction S.  Readings
+ * (R15-R18): at size n, B r = e + alpha h*(A^T (r - A e)) with
+ * e = P B_{n/2}(S r) and alpha = <r', A p> / <A p, A p> (r' the remainder, p the
+ * filtered backprojection: the residual-minimising step); at n = n_min,
+ * B r = alpha h*(A^T r).  h uses zero padding.  n_min = N is the single-grid
+ * iteration x <- x + alpha h*(A^T r).
+ * coef: [K][N][N][3N] fp32 device (the stacked forward layout, K = popcount
+ * of the mask); n_min: coarsest grid, a power of two in [2, N]; cube: [N][N][N]
+ * fp32 device, receives x_iters; rnorm: NULL or a device array of iters+1
+ * doubles receiving ||b - A x_k||_2, k = 0..iters.
+ * opts: NULL or batch = 1, out_dtype = F32, STACKED (in_dtype ignored).
+ * Workspace: per level n = N, N/2, .., n_min four coefficient-sized and three
+ * cube-sized fp32 buffers, plus the larger of the size-N forward / adjoint
+ * workspaces (query the size; 256-byte aligned).
+ * Enqueue only: every iteration runs on `stream` with no host synchronisation
+ * (the step sizes live in the workspace).
+ * Errors: DRT3D_ERR_INVALID_ARG (N, n_min, mask, opts, NULL pointers,
+ * iters < 0), DRT3D_ERR_WORKSPACE, DRT3D_ERR_CUDA.                           */
+drt3d_status drt3d_planes_invert_workspace_size(int N, int n_min, uint32_t dodecant_mask,
+                                                const drt3d_opts *opts, size_t *bytes);
+drt3d_status drt3d_planes_invert(const void *coef, int N, int n_min, uint32_t dodecant_mask, int iters,
+                                 void *cube, double *rnorm, const drt3d_opts *opts, void *workspace,
+                                 size_t workspace_bytes, void *stream);
+
 /* --------------------------------------------------------- host buffers --
  * End-to-end variants: `host_cube` and `host_out` are HOST pointers (pinned
  * for full speed); `dev_cube` (>= cube bytes), `dev_out` (>= out bytes) and

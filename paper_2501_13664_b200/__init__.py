@@ -27,7 +27,8 @@ C_FUNCTIONS = ("drt3d_status_string", "drt3d_orientation_table", "drt3d_planes_o
                "drt3d_planes_workspace_size", "drt3d_planes", "djt3d_lines_out_elems",
                "djt3d_lines_workspace_size", "djt3d_lines", "drt3d_planes_host", "djt3d_lines_host",
                "drt3d_planes_adjoint_workspace_size", "drt3d_planes_adjoint",
-               "djt3d_lines_adjoint_workspace_size", "djt3d_lines_adjoint")
+               "djt3d_lines_adjoint_workspace_size", "djt3d_lines_adjoint",
+               "drt3d_planes_invert_workspace_size", "drt3d_planes_invert")
 
 
 class Drt3dError(RuntimeError):
@@ -78,6 +79,10 @@ def lib() -> ctypes.CDLL:
         f = getattr(L, t + "_adjoint")
         f.restype = i32
         f.argtypes = [vp, i32, u32, vp, po, vp, sz, vp]
+    L.drt3d_planes_invert_workspace_size.restype = i32
+    L.drt3d_planes_invert_workspace_size.argtypes = [i32, i32, u32, po, ctypes.POINTER(sz)]
+    L.drt3d_planes_invert.restype = i32
+    L.drt3d_planes_invert.argtypes = [vp, i32, i32, u32, i32, vp, vp, po, vp, sz, vp]
     _lib = L
     return L
 
@@ -255,3 +260,33 @@ def lines_adjoint(coef, mask: int = 0x001, table: int = DRT3D_TABLE_HEMISPHERE, 
                   stream=None, opts: drt3d_opts | None = None):
     """Backprojection of stacked DJT coefficients [B,K,N,N,2N,2N] (int32 / float32) -> [B,N,N,N]."""
     return _adjoint("djt", coef, mask, table, cube, workspace, stream, opts)
+
+
+# ------------------------------------------------------- iterative inverse (F-3)
+
+def planes_invert(coef, iters: int, mask: int = 0xFFF, n_min: int = 2, table: int = DRT3D_TABLE_HEMISPHERE,
+                  cube=None, workspace=None, stream=None, opts: drt3d_opts | None = None):
+    """Iterative inverse of stacked fp32 DRT coefficients [K,N,N,3N] -> (x [N,N,N] fp32,
+    rnorm [iters+1] fp64 residual norms ||b - A x_k||) by drt3d_planes_invert (DESIGN.md F-3);
+    n_min = coarsest multigrid size (n_min = N: single-grid iteration)."""
+    import torch
+    if not coef.is_cuda or coef.dtype != torch.float32 or coef.dim() != 4:
+        raise Drt3dError("coef must be a CUDA float32 tensor [K,N,N,3N]")
+    c = coef.contiguous()
+    N = c.shape[1]
+    o = make_opts(batch=1, in_dtype=DRT3D_F32, out_dtype=DRT3D_F32, table=table)
+    if opts is not None:
+        o.launches = opts.launches
+    if cube is None:
+        cube = torch.empty((N, N, N), dtype=torch.float32, device=c.device)
+    rnorm = torch.empty(iters + 1, dtype=torch.float64, device=c.device)
+    L = lib()
+    b = ctypes.c_size_t(0)
+    _check(L.drt3d_planes_invert_workspace_size(N, n_min, mask, ctypes.byref(o), ctypes.byref(b)),
+           "invert_workspace_size")
+    if workspace is None:
+        workspace = torch.empty(max(b.value, 256), dtype=torch.uint8, device=c.device)
+    st = stream if stream is not None else torch.cuda.current_stream(c.device).cuda_stream
+    _check(L.drt3d_planes_invert(c.data_ptr(), N, n_min, mask, iters, cube.data_ptr(), rnorm.data_ptr(), ctypes.byref(o),
+                                 workspace.data_ptr(), b.value, st), "planes invert")
+    return cube, rnorm

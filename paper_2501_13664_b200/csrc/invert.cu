@@ -1,0 +1,367 @@
+// invert.cu -- iterative inverse of the 3D DRT of planes.
+//
+// the adjoint is used "as an approximate inverse operator of the DRT in the
+// theory of iterative improvement of a solution to linear equations" (Press, Numerical Recipes
+// §2.5), x <- x + B (b - A x), with the 3D high-pass filter h of PAPER.md:576-591 and the
+// prolongation P / restriction S multigrid of PAPER.md:592-601.  Readings (R15-R18):
+// the filtered-backprojection step is alpha h*(A^T r) with alpha = <r, A p> / <A p, A p>,
+// p = h*(A^T r) (residual-minimising); h with zero padding; B (mg_apply) = restrict the residual,
+// recurse to N/2, prolongate, then one filtered-backprojection step on what remains; the
+// coarsest size n_min takes the step alone (n_min = N: single-grid iteration).
+//
+// Every iteration is enqueued on the caller's stream with no host synchronisation: A^T is the
+// library's backprojection, A its forward transform (fp32 in / fp32 out), and alpha is computed
+// on the device by a fixed-order two-pass fp64 reduction (deterministic) and read by the update
+// kernels from device memory.
+#include "drt3d.h"
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace d3 {
+namespace inv {
+
+constexpr int kRedBlocks = 592;      // 4 x 148 SMs, fixed so the reduction order is fixed
+constexpr int kRedThreads = 256;
+
+__device__ __forceinline__ double block_sum(double v, double *sh) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (threadIdx.x < 32) {
+        t = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    }
+    return t;                                   // valid in thread 0
+}
+
+// part[2 blk] = sum r*q, part[2 blk + 1] = sum q*q over this block's grid-stride share
+__global__ void __launch_bounds__(kRedThreads) dot_rq_qq(const float *__restrict__ r, const float *__restrict__ q,
+                                                          size_t n, double *__restrict__ part) {
+    __shared__ double sh[2][kRedThreads / 32];
+    double rq = 0.0, qq = 0.0;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const double a = r[i], b = q[i];
+        rq += a * b;
+        qq += b * b;
+    }
+    const double s0 = block_sum(rq, sh[0]);
+    const double s1 = block_sum(qq, sh[1]);
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = s0;
+        part[2 * blockIdx.x + 1] = s1;
+    }
+}
+
+// alpha = (sum rq) / (sum qq), 0 when A p = 0
+__global__ void finalize_alpha(const double *__restrict__ part, int nb, double *__restrict__ alpha) {
+    __shared__ double sh[2][kRedThreads / 32];
+    double rq = 0.0, qq = 0.0;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+        rq += part[2 * i];
+        qq += part[2 * i + 1];
+    }
+    const double s0 = block_sum(rq, sh[0]);
+    const double s1 = block_sum(qq, sh[1]);
+    if (threadIdx.x == 0) *alpha = s1 > 0.0 ? s0 / s1 : 0.0;
+}
+
+// r <- r - alpha q (fp32), part[blk] = sum r_new^2
+__global__ void __launch_bounds__(kRedThreads) update_r(float *__restrict__ r, const float *__restrict__ q, size_t n,
+                                                         const double *__restrict__ alpha, double *__restrict__ part) {
+    __shared__ double sh[kRedThreads / 32];
+    const float a = (float)*alpha;
+    double rr = 0.0;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const float v = r[i] - a * q[i];
+        r[i] = v;
+        rr += (double)v * v;
+    }
+    const double s = block_sum(rr, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// part[blk] = sum r^2 (initial residual norm)
+__global__ void __launch_bounds__(kRedThreads) sum_sq(const float *__restrict__ r, size_t n, double *__restrict__ part) {
+    __shared__ double sh[kRedThreads / 32];
+    double rr = 0.0;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const double v = r[i];
+        rr += v * v;
+    }
+    const double s = block_sum(rr, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void finalize_norm(const double *__restrict__ part, int nb, double *__restrict__ out) {
+    __shared__ double sh[kRedThreads / 32];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) s += part[i];
+    const double t = block_sum(s, sh);
+    if (threadIdx.x == 0 && out) *out = sqrt(t);
+}
+
+// x <- x + alpha p
+__global__ void update_x(float *__restrict__ x, const float *__restrict__ p, size_t n,
+                         const double *__restrict__ alpha) {
+    const float a = (float)*alpha;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        x[i] = x[i] + a * p[i];
+}
+
+// p = h * g, h of PAPER.md:576-591 (centre 7/8, faces -1/16, edges -1/32, corners -1/64), zero
+// outside the cube.  grid.x = x * N + y, threads along z.
+__global__ void highpass(const float *__restrict__ g, float *__restrict__ p, int N) {
+    const int x = blockIdx.x / N, y = blockIdx.x - x * N;
+    const float w[4] = {7.f / 8.f, -1.f / 16.f, -1.f / 32.f, -1.f / 64.f};
+    for (int z = threadIdx.x; z < N; z += blockDim.x) {
+        float acc = 0.f;
+#pragma unroll
+        for (int a = -1; a <= 1; ++a) {
+            if (x + a < 0 || x + a >= N) continue;
+#pragma unroll
+            for (int b = -1; b <= 1; ++b) {
+                if (y + b < 0 || y + b >= N) continue;
+                const float *row = g + ((size_t)(x + a) * N + (y + b)) * N;
+#pragma unroll
+                for (int c = -1; c <= 1; ++c) {
+                    if (z + c < 0 || z + c >= N) continue;
+                    acc += w[(a != 0) + (b != 0) + (c != 0)] * __ldg(row + z + c);
+                }
+            }
+        }
+        p[((size_t)x * N + y) * N + z] = acc;
+    }
+}
+
+// S: rc[k][s1][s2][d] = (r[k][2 s1][2 s2][2 d] + r[k][2 s1][2 s2][2 d + 1]) / 8,
+// coarse size nc (fine 2 nc).  grid.x = k * nc * nc + s1 * nc + s2, threads along d.
+__global__ void restrict_coef(const float *__restrict__ r, float *__restrict__ rc, int nc) {
+    const int Wc = 3 * nc, W = 6 * nc, n = 2 * nc;
+    const int row = blockIdx.x, k = row / (nc * nc), s1 = (row / nc) % nc, s2 = row % nc;
+    const float *src = r + (((size_t)k * n + 2 * s1) * n + 2 * s2) * W;
+    float *dst = rc + (size_t)row * Wc;
+    for (int d = threadIdx.x; d < Wc; d += blockDim.x) dst[d] = 0.125f * (src[2 * d] + src[2 * d + 1]);
+}
+
+// P: e[x][y][z] = ec[x/2][y/2][z/2].  grid.x = x * n + y, threads along z.
+__global__ void prolong_cube(const float *__restrict__ ec, float *__restrict__ e, int n) {
+    const int x = blockIdx.x / n, y = blockIdx.x % n, nc = n / 2;
+    const float *src = ec + ((size_t)(x / 2) * nc + y / 2) * nc;
+    float *dst = e + (size_t)blockIdx.x * n;
+    for (int z = threadIdx.x; z < n; z += blockDim.x) dst[z] = src[z / 2];
+}
+
+// out = a - b
+__global__ void diff(const float *__restrict__ a, const float *__restrict__ b, float *__restrict__ out, size_t n) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        out[i] = a[i] - b[i];
+}
+
+inline size_t align256(size_t b) { return (b + 255) / 256 * 256; }
+
+constexpr int kMaxLevels = 11;
+
+// Per grid level (0 = the caller's size N, level l has size N >> l): residual r, its remainder
+// rp = r - A e, A e, A p (coefficient-sized); e, A^T rp, p (cube-sized).  Level 0's r is the
+// outer residual.
+struct Level {
+    int n;
+    size_t ncoef, ncube;
+    size_t r, rp, ae, q, e, g, p;
+};
+
+struct Layout {
+    int nlev;
+    Level lv[kMaxLevels];
+    size_t part, scal, tws, total, tws_bytes;
+};
+
+inline drt3d_opts f32_opts(int table) {
+    drt3d_opts o = {};
+    o.batch = 1;
+    o.in_dtype = DRT3D_F32;
+    o.out_dtype = DRT3D_F32;
+    o.layout = DRT3D_LAYOUT_STACKED;
+    o.table = table;
+    return o;
+}
+
+inline drt3d_status layout(int N, int n_min, uint32_t mask, int table, Layout &L) {
+    const int K = __builtin_popcount(mask & 0xFFFu);
+    drt3d_opts o = f32_opts(table);
+    size_t fw = 0, aw = 0;
+    drt3d_status s = drt3d_planes_workspace_size(N, mask, &o, &fw);       // the largest level's
+    if (s != DRT3D_OK) return s;
+    s = drt3d_planes_adjoint_workspace_size(N, mask, &o, &aw);
+    if (s != DRT3D_OK) return s;
+    L.tws_bytes = align256(fw > aw ? fw : aw);          // forward and adjoint run one after the other
+    size_t off = 0;
+    L.nlev = 0;
+    for (int n = N; n >= n_min && L.nlev < kMaxLevels; n >>= 1) {
+        Level &v = L.lv[L.nlev++];
+        v.n = n;
+        v.ncoef = (size_t)K * n * n * 3 * n;
+        v.ncube = (size_t)n * n * n;
+        v.r = off; off += align256(v.ncoef * 4);
+        v.rp = off; off += align256(v.ncoef * 4);
+        v.ae = off; off += align256(v.ncoef * 4);
+        v.q = off; off += align256(v.ncoef * 4);
+        v.e = off; off += align256(v.ncube * 4);
+        v.g = off; off += align256(v.ncube * 4);
+        v.p = off; off += align256(v.ncube * 4);
+    }
+    L.part = off; off += align256(2 * kRedBlocks * sizeof(double));
+    L.scal = off; off += 256;                           // [0] = 1.0, [1 + l] = alpha of level l
+    L.tws = off; off += L.tws_bytes;
+    L.total = off;
+    return DRT3D_OK;
+}
+
+}  // namespace inv
+}  // namespace d3
+
+using namespace d3::inv;
+
+static drt3d_status invert_check(int N, int n_min, uint32_t mask, const drt3d_opts *opts, int &table) {
+    if (N < 2 || N > 1024 || (N & (N - 1)) || mask == 0 || mask >= (1u << 12)) return DRT3D_ERR_INVALID_ARG;
+    if (n_min < 2 || n_min > N || (n_min & (n_min - 1))) return DRT3D_ERR_INVALID_ARG;
+    table = DRT3D_TABLE_HEMISPHERE;
+    if (opts) {
+        if (opts->batch != 1 || opts->out_dtype != DRT3D_F32 || opts->layout != DRT3D_LAYOUT_STACKED)
+            return DRT3D_ERR_INVALID_ARG;
+        if (opts->table < 0 || opts->table > 2) return DRT3D_ERR_INVALID_ARG;
+        table = opts->table;
+    }
+    return DRT3D_OK;
+}
+
+extern "C" drt3d_status drt3d_planes_invert_workspace_size(int N, int n_min, uint32_t mask, const drt3d_opts *opts,
+                                                           size_t *bytes) {
+    int table;
+    if (!bytes) return DRT3D_ERR_INVALID_ARG;
+    drt3d_status s = invert_check(N, n_min, mask, opts, table);
+    if (s != DRT3D_OK) return s;
+    Layout L;
+    s = layout(N, n_min, mask, table, L);
+    if (s != DRT3D_OK) return s;
+    *bytes = L.total;
+    return DRT3D_OK;
+}
+
+namespace {
+
+struct Ctx {
+    const Layout *L;
+    unsigned char *w;
+    uint32_t mask;
+    cudaStream_t st;
+    void *stream;
+    drt3d_opts o;
+    int nl;
+    float *f(size_t off) const { return reinterpret_cast<float *>(w + off); }
+    double *part() const { return reinterpret_cast<double *>(w + L->part); }
+    double *one() const { return reinterpret_cast<double *>(w + L->scal); }
+    double *alpha(int l) const { return reinterpret_cast<double *>(w + L->scal) + 1 + l; }
+    void *tws() const { return w + L->tws; }
+};
+
+inline unsigned row_threads(int len) { return len >= 128 ? 128u : (unsigned)((len + 31) / 32 * 32); }
+
+// R16 step on residual `res` at level l: p = h*(A^T res), q = A p, alpha_l = <res,q>/<q,q>.
+drt3d_status step(Ctx &c, int l, const float *res) {
+    const Level &v = c.L->lv[l];
+    int l1 = 0, l2 = 0;
+    c.o.launches = &l1;
+    drt3d_status s = drt3d_planes_adjoint(res, v.n, c.mask, c.f(v.g), &c.o, c.tws(), c.L->tws_bytes, c.stream);
+    if (s != DRT3D_OK) return s;
+    highpass<<<(unsigned)(v.n * v.n), row_threads(v.n), 0, c.st>>>(c.f(v.g), c.f(v.p), v.n);
+    c.o.launches = &l2;
+    s = drt3d_planes(c.f(v.p), v.n, c.mask, c.f(v.q), &c.o, c.tws(), c.L->tws_bytes, c.stream);
+    if (s != DRT3D_OK) return s;
+    dot_rq_qq<<<kRedBlocks, kRedThreads, 0, c.st>>>(res, c.f(v.q), v.ncoef, c.part());
+    finalize_alpha<<<1, kRedThreads, 0, c.st>>>(c.part(), kRedBlocks, c.alpha(l));
+    c.nl += l1 + l2 + 3;
+    return DRT3D_OK;
+}
+
+// Multigrid approximate inverse (R18) of the residual in level l's `r` buffer: leaves e_l = B r_l
+// in `e` and A e_l in `ae`.
+drt3d_status mg_apply(Ctx &c, int l) {
+    const Level &v = c.L->lv[l];
+    const unsigned nb = kRedBlocks;
+    if (l == c.L->nlev - 1) {                                    // coarsest: e = alpha p, ae = alpha q
+        drt3d_status s = step(c, l, c.f(v.r));
+        if (s != DRT3D_OK) return s;
+        if (cudaMemsetAsync(c.f(v.e), 0, v.ncube * 4, c.st) != cudaSuccess) return DRT3D_ERR_CUDA;
+        if (cudaMemsetAsync(c.f(v.ae), 0, v.ncoef * 4, c.st) != cudaSuccess) return DRT3D_ERR_CUDA;
+        update_x<<<nb, kRedThreads, 0, c.st>>>(c.f(v.e), c.f(v.p), v.ncube, c.alpha(l));
+        update_x<<<nb, kRedThreads, 0, c.st>>>(c.f(v.ae), c.f(v.q), v.ncoef, c.alpha(l));
+        c.nl += 2;
+        return DRT3D_OK;
+    }
+    const Level &u = c.L->lv[l + 1];
+    const int K = (int)(v.ncoef / ((size_t)v.n * v.n * 3 * v.n));
+    restrict_coef<<<(unsigned)(K * u.n * u.n), row_threads(3 * u.n), 0, c.st>>>(c.f(v.r), c.f(u.r), u.n);  // S r
+    c.nl += 1;
+    drt3d_status s = mg_apply(c, l + 1);                                                                    // B_{n/2}
+    if (s != DRT3D_OK) return s;
+    prolong_cube<<<(unsigned)(v.n * v.n), row_threads(v.n), 0, c.st>>>(c.f(u.e), c.f(v.e), v.n);          // e = P e_c
+    int l1 = 0;
+    c.o.launches = &l1;
+    s = drt3d_planes(c.f(v.e), v.n, c.mask, c.f(v.ae), &c.o, c.tws(), c.L->tws_bytes, c.stream);         // A e
+    if (s != DRT3D_OK) return s;
+    diff<<<nb, kRedThreads, 0, c.st>>>(c.f(v.r), c.f(v.ae), c.f(v.rp), v.ncoef);                          // r' = r - A e
+    c.nl += l1 + 2;
+    s = step(c, l, c.f(v.rp));
+    if (s != DRT3D_OK) return s;
+    update_x<<<nb, kRedThreads, 0, c.st>>>(c.f(v.e), c.f(v.p), v.ncube, c.alpha(l));                       // e += a p
+    update_x<<<nb, kRedThreads, 0, c.st>>>(c.f(v.ae), c.f(v.q), v.ncoef, c.alpha(l));                      // Ae += a q
+    c.nl += 2;
+    return DRT3D_OK;
+}
+
+}  // namespace
+
+extern "C" drt3d_status drt3d_planes_invert(const void *coef, int N, int n_min, uint32_t mask, int iters, void *cube,
+                                            double *rnorm, const drt3d_opts *opts, void *ws, size_t ws_bytes,
+                                            void *stream) {
+    int table;
+    drt3d_status s = invert_check(N, n_min, mask, opts, table);
+    if (s != DRT3D_OK) return s;
+    if (!coef || !cube || iters < 0) return DRT3D_ERR_INVALID_ARG;
+    Layout L;
+    s = layout(N, n_min, mask, table, L);
+    if (s != DRT3D_OK) return s;
+    if (!ws || ws_bytes < L.total || (reinterpret_cast<uintptr_t>(ws) & 255)) return DRT3D_ERR_WORKSPACE;
+    Ctx c{&L, reinterpret_cast<unsigned char *>(ws), mask, reinterpret_cast<cudaStream_t>(stream), stream,
+          f32_opts(table), 0};
+    const Level &top = L.lv[0];
+    float *x = reinterpret_cast<float *>(cube), *r = c.f(top.r);
+    static const double kOne = 1.0;
+    if (cudaMemcpyAsync(c.one(), &kOne, sizeof(double), cudaMemcpyHostToDevice, c.st) != cudaSuccess)
+        return DRT3D_ERR_CUDA;
+    // x0 = 0, r0 = b
+    if (cudaMemsetAsync(x, 0, top.ncube * 4, c.st) != cudaSuccess) return DRT3D_ERR_CUDA;
+    if (cudaMemcpyAsync(r, coef, top.ncoef * 4, cudaMemcpyDeviceToDevice, c.st) != cudaSuccess) return DRT3D_ERR_CUDA;
+    if (rnorm) {
+        sum_sq<<<kRedBlocks, kRedThreads, 0, c.st>>>(r, top.ncoef, c.part());
+        finalize_norm<<<1, kRedThreads, 0, c.st>>>(c.part(), kRedBlocks, rnorm);
+        c.nl += 2;
+    }
+    for (int k = 0; k < iters; ++k) {
+        s = mg_apply(c, 0);                                                              // e = B r, A e
+        if (s != DRT3D_OK) return s;
+        update_x<<<kRedBlocks, kRedThreads, 0, c.st>>>(x, c.f(top.e), top.ncube, c.one());           // x += e
+        update_r<<<kRedBlocks, kRedThreads, 0, c.st>>>(r, c.f(top.ae), top.ncoef, c.one(), c.part()); // r -= A e
+        finalize_norm<<<1, kRedThreads, 0, c.st>>>(c.part(), kRedBlocks, rnorm ? rnorm + k + 1 : nullptr);
+        c.nl += 3;
+    }
+    if (opts && opts->launches) *opts->launches = c.nl;
+    return cudaGetLastError() == cudaSuccess ? DRT3D_OK : DRT3D_ERR_CUDA;
+}

@@ -4,6 +4,7 @@ Inputs are the seeded synthetic cubes of synth/ (DESIGN.md §4), resident in HBM
 timed with CUDA events on the launching stream after 3 warm-ups, median of 10 (a 512 MB L2 flush
 between calls).  Prints one JSON object per config; the headline line is bench.py's (config 3).
 """
+import ctypes
 import json
 import os
 import statistics
@@ -93,6 +94,35 @@ def run_adjoint(cfg, iters=5):
             "coef_read_gbs": coef.numel() * 4 / (ms * 1e-3) / 1e9}
 
 
+def run_invert(N, iters=6):
+    """Iterative inverse (F-3): `iters` multigrid iterations (n_min = 2) over all 12 dodecants,
+    fp32, on a smooth synthetic phantom."""
+    x, y, z = torch.meshgrid(*[torch.arange(N, dtype=torch.float32, device="cuda")] * 3, indexing="ij")
+    f = torch.exp(-((x - 0.45 * N) ** 2 / (0.12 * N * N) + (y - 0.55 * N) ** 2 / (0.15 * N * N)
+                    + (z - 0.5 * N) ** 2 / (0.18 * N * N)))
+    b = d3.planes(f[None].contiguous(), 0xFFF)[0]
+    o = d3.make_opts(batch=1, in_dtype=d3.DRT3D_F32, out_dtype=d3.DRT3D_F32)
+    wsb = ctypes.c_size_t(0)
+    d3.lib().drt3d_planes_invert_workspace_size(N, 2, 0xFFF, ctypes.byref(o), ctypes.byref(wsb))
+    ws = torch.empty(wsb.value, dtype=torch.uint8, device="cuda")
+    cube = torch.empty((N, N, N), dtype=torch.float32, device="cuda")
+    d3.planes_invert(b, 1, cube=cube, workspace=ws)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(3):
+        a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        _, rn = d3.planes_invert(b, iters, cube=cube, workspace=ws)
+        e.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(e))
+    ms = statistics.median(ts)
+    err = float(torch.linalg.norm(cube - f) / torch.linalg.norm(f))
+    return {"config": f"invert-N{N}", "transform": "drt_invert", "N": N, "iters": iters, "dodecants": 12,
+            "ms_median": ms, "ms_per_iter": ms / iters, "nrmsd": err,
+            "rnorm_ratio": float(rn[-1] / rn[0]), "workspace_mb": wsb.value / 2 ** 20}
+
+
 if __name__ == "__main__":
     cfgs = [int(a) for a in sys.argv[1:]] or [1, 2, 3, 4, 5]
     for c in cfgs:
@@ -100,3 +130,5 @@ if __name__ == "__main__":
     if len(sys.argv) == 1:
         for c in (3, 4):
             print(json.dumps(run_adjoint(c)), flush=True)
+        for n in (64, 128, 256):
+            print(json.dumps(run_invert(n)), flush=True)
