@@ -165,6 +165,35 @@ drt3d_status drt3d_planes_invert(const void *coef, int N, int n_min, uint32_t do
                                  void *cube, double *rnorm, const drt3d_opts *opts, void *workspace,
                                  size_t workspace_bytes, void *stream);
 
+/* --------------------------------------------------------- applications --
+ * SURVEY §8(f) F-4, on int32 coefficient arrays in device memory (any layout
+ * for argmax / threshold; the stacked DRT layout [K][N][N][3N] for planes).
+ * Workspace: drt3d_apps_workspace_size() bytes, 256-byte aligned, device.
+ * All enqueue on `stream`; results are deterministic (fixed-order reductions).
+ *
+ * drt3d_coef_argmax: *index (device int64) = flat index of the largest
+ *   coefficient, the smallest index among ties (R20).
+ * drt3d_coef_threshold: out[i] = coef[i] if coef[i] * den >= num * max(coef)
+ *   else 0, tested exactly in int64 (R19; "a thresholding of the
+ *   highest amplitude coefficients, and subsequent backprojection"); out may
+ *   alias coef.  num >= 0, den > 0.
+ * drt3d_detect_planes: flags[i] (device uint8, same shape
+ *   as coef) = 1 for the argmax plane and for every coefficient that passes
+ *   the R19 threshold, is a relative maximum of its dodecant's (s1, s2, D)
+ *   26-neighbourhood (R21) and whose plane is orthogonal to the argmax plane,
+ *   |cos| <= onum/oden, with integer normals through the orientation table
+ *   opts->table (R22); *argmax (device int64, may be NULL) receives R20's index.
+ * Errors: DRT3D_ERR_INVALID_ARG (NULL pointers, n = 0, N, mask, num < 0,
+ *   den <= 0, onum < 0, oden <= 0), DRT3D_ERR_WORKSPACE, DRT3D_ERR_CUDA.      */
+size_t drt3d_apps_workspace_size(void);
+drt3d_status drt3d_coef_argmax(const int32_t *coef, size_t n, long long *index, void *workspace,
+                               size_t workspace_bytes, void *stream);
+drt3d_status drt3d_coef_threshold(const int32_t *coef, size_t n, int num, int den, int32_t *out,
+                                  void *workspace, size_t workspace_bytes, void *stream);
+drt3d_status drt3d_detect_planes(const int32_t *coef, int N, uint32_t dodecant_mask, int num, int den,
+                                 int onum, int oden, const drt3d_opts *opts, uint8_t *flags,
+                                 long long *argmax, void *workspace, size_t workspace_bytes, void *stream);
+
 /* --------------------------------------------------------- host buffers --
  * End-to-end variants: `host_cube` and `host_out` are HOST pointers (pinned
  * for full speed); `dev_cube` (>= cube bytes), `dev_out` (>= out bytes) and

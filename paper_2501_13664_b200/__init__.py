@@ -28,7 +28,8 @@ C_FUNCTIONS = ("drt3d_status_string", "drt3d_orientation_table", "drt3d_planes_o
                "djt3d_lines_workspace_size", "djt3d_lines", "drt3d_planes_host", "djt3d_lines_host",
                "drt3d_planes_adjoint_workspace_size", "drt3d_planes_adjoint",
                "djt3d_lines_adjoint_workspace_size", "djt3d_lines_adjoint",
-               "drt3d_planes_invert_workspace_size", "drt3d_planes_invert")
+               "drt3d_planes_invert_workspace_size", "drt3d_planes_invert",
+               "drt3d_apps_workspace_size", "drt3d_coef_argmax", "drt3d_coef_threshold", "drt3d_detect_planes")
 
 
 class Drt3dError(RuntimeError):
@@ -83,6 +84,14 @@ def lib() -> ctypes.CDLL:
     L.drt3d_planes_invert_workspace_size.argtypes = [i32, i32, u32, po, ctypes.POINTER(sz)]
     L.drt3d_planes_invert.restype = i32
     L.drt3d_planes_invert.argtypes = [vp, i32, i32, u32, i32, vp, vp, po, vp, sz, vp]
+    L.drt3d_apps_workspace_size.restype = sz
+    L.drt3d_apps_workspace_size.argtypes = []
+    L.drt3d_coef_argmax.restype = i32
+    L.drt3d_coef_argmax.argtypes = [vp, sz, vp, vp, sz, vp]
+    L.drt3d_coef_threshold.restype = i32
+    L.drt3d_coef_threshold.argtypes = [vp, sz, i32, i32, vp, vp, sz, vp]
+    L.drt3d_detect_planes.restype = i32
+    L.drt3d_detect_planes.argtypes = [vp, i32, u32, i32, i32, i32, i32, po, vp, vp, vp, sz, vp]
     _lib = L
     return L
 
@@ -290,3 +299,57 @@ def planes_invert(coef, iters: int, mask: int = 0xFFF, n_min: int = 2, table: in
     _check(L.drt3d_planes_invert(c.data_ptr(), N, n_min, mask, iters, cube.data_ptr(), rnorm.data_ptr(), ctypes.byref(o),
                                  workspace.data_ptr(), b.value, st), "planes invert")
     return cube, rnorm
+
+
+# ------------------------------------------------------------ applications (F-4)
+
+def _apps_ws(device):
+    import torch
+    return torch.empty(max(lib().drt3d_apps_workspace_size(), 256), dtype=torch.uint8, device=device)
+
+
+def coef_argmax(coef, workspace=None, stream=None) -> int:
+    """Flat index of the largest int32 coefficient (smallest index among ties); synchronises."""
+    import torch
+    c = coef.contiguous()
+    if not c.is_cuda or c.dtype != torch.int32:
+        raise Drt3dError("coef must be a CUDA int32 tensor")
+    ws = workspace if workspace is not None else _apps_ws(c.device)
+    idx = torch.empty(1, dtype=torch.int64, device=c.device)
+    st = stream if stream is not None else torch.cuda.current_stream(c.device).cuda_stream
+    _check(lib().drt3d_coef_argmax(c.data_ptr(), c.numel(), idx.data_ptr(), ws.data_ptr(), ws.numel(), st),
+           "coef_argmax")
+    return int(idx.item())
+
+
+def coef_threshold(coef, num: int, den: int, out=None, workspace=None, stream=None):
+    """Keep c where c * den >= num * max(c), else 0 (int32, exact)."""
+    import torch
+    c = coef.contiguous()
+    if not c.is_cuda or c.dtype != torch.int32:
+        raise Drt3dError("coef must be a CUDA int32 tensor")
+    out = torch.empty_like(c) if out is None else out
+    ws = workspace if workspace is not None else _apps_ws(c.device)
+    st = stream if stream is not None else torch.cuda.current_stream(c.device).cuda_stream
+    _check(lib().drt3d_coef_threshold(c.data_ptr(), c.numel(), num, den, out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                      st), "coef_threshold")
+    return out
+
+
+def detect_planes(coef, mask: int, num: int, den: int, onum: int, oden: int, table: int = DRT3D_TABLE_HEMISPHERE,
+                  workspace=None, stream=None):
+    """Plane detection on stacked int32 DRT coefficients [K,N,N,3N] -> (flags uint8 [K,N,N,3N],
+    argmax flat index tensor [1] int64), F-4."""
+    import torch
+    c = coef.contiguous()
+    if not c.is_cuda or c.dtype != torch.int32 or c.dim() != 4:
+        raise Drt3dError("coef must be a CUDA int32 tensor [K,N,N,3N]")
+    N = c.shape[1]
+    flags = torch.empty(c.shape, dtype=torch.uint8, device=c.device)
+    am = torch.empty(1, dtype=torch.int64, device=c.device)
+    o = make_opts(table=table)
+    ws = workspace if workspace is not None else _apps_ws(c.device)
+    st = stream if stream is not None else torch.cuda.current_stream(c.device).cuda_stream
+    _check(lib().drt3d_detect_planes(c.data_ptr(), N, mask, num, den, onum, oden, ctypes.byref(o), flags.data_ptr(),
+                                     am.data_ptr(), ws.data_ptr(), ws.numel(), st), "detect_planes")
+    return flags, am

@@ -72,3 +72,39 @@ def test_drt_adjoint_identity_gpu(N):
     rhs = int((f.to(torch.int64) * atc.to(torch.int64)).sum())
     # no int32 wrap here: |A f| <= 255 N^2 and |A^T c| <= 3 K N^2 * 3 < 2^31, so both sides are exact
     assert lhs == rhs
+
+
+@pytest.mark.parametrize("N", [16, 32, 64, 128])
+def test_djt_adjoint_single_line_closed_form(N):
+    """A^T of one unit coefficient (s1, s2, D1, D2) is the indicator of that digital line
+    (eq:3DfDJT): voxels (u, l_s1(u) + D1 - N, l_s2(u) + D2 - N) inside the cube."""
+    n = N.bit_length() - 1
+    cases = [(0, 0, N, N), (N - 1, N - 1, N, N), (N // 3, 2 * N // 3, N + 5, N + 1), (1, N - 2, 3, 2 * N - 2)]
+    for (s1, s2, D1, D2) in cases:
+        c = torch.zeros((1, 1, N, N, 2 * N, 2 * N), dtype=torch.int32, device="cuda")
+        c[0, 0, s1, s2, D1, D2] = 1
+        got = d3.lines_adjoint(c, 0x001)[0].cpu().numpy()
+        ref = np.zeros((N, N, N), np.int64)
+        for u in range(N):
+            y, z = oracle.line(n, s1, u) + D1 - N, oracle.line(n, s2, u) + D2 - N
+            if 0 <= y < N and 0 <= z < N:
+                ref[u, y, z] = 1
+        assert np.array_equal(got.astype(np.int64), ref), (s1, s2, D1, D2)
+
+
+@pytest.mark.parametrize("N", [32, 64, 128])
+def test_drt_adjoint_single_plane_closed_form(N):
+    """A^T of one unit coefficient (s1, s2, D) of dodecant 0 is the indicator of that digital
+    plane (eq:3DfDRT, PAPER.md:193-198): voxels (x, y, l_s1(x) + l_s2(y) + D - 2N) inside."""
+    n = N.bit_length() - 1
+    for (s1, s2, D) in [(0, 0, 2 * N + 3), (N - 1, 1, 2 * N - 5), (N // 3, 2 * N // 3, N + 7)]:
+        c = torch.zeros((1, 1, N, N, 3 * N), dtype=torch.int32, device="cuda")
+        c[0, 0, s1, s2, D] = 1
+        got = d3.planes_adjoint(c, 0x001)[0].cpu().numpy()
+        ref = np.zeros((N, N, N), np.int64)
+        for x in range(N):
+            for y in range(N):
+                z = oracle.line(n, s1, x) + oracle.line(n, s2, y) + D - 2 * N
+                if 0 <= z < N:
+                    ref[x, y, z] = 1
+        assert np.array_equal(got.astype(np.int64), ref), (s1, s2, D)

@@ -123,6 +123,56 @@ def run_invert(N, iters=6):
             "rnorm_ratio": float(rn[-1] / rn[0]), "workspace_mb": wsb.value / 2 ** 20}
 
 
+def _time(fn, iters=5):
+    fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(iters):
+        a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        e.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(e))
+    return statistics.median(ts)
+
+
+def run_apps():
+    """F-4: plane detection on a synthetic 128^3 room (PAPER.md:679's scene size: three walls, a box,
+    0.5% clutter), and ray denoising (DJT dodecant 0 -> threshold 0.95 max -> backprojection) at N=64."""
+    import numpy as np
+    N = 128
+    rng = np.random.default_rng(5)
+    f = np.zeros((N, N, N), np.uint8)
+    f[3, :, :] = 1
+    f[:, N - 4, :] = 1
+    f[:, :, 2] = 1
+    f[N // 3:N // 2, N // 3:N // 2, N // 3:N // 2] = 1
+    f = (f + (rng.random((N, N, N)) < 0.005)).astype(np.uint8)
+    cube = torch.from_numpy(f).cuda()
+    c = d3.planes(cube, 0xFFF)
+    ws = d3._apps_ws(c.device)
+    t_fwd = _time(lambda: d3.planes(cube, 0xFFF, out=c))
+    t_det = _time(lambda: d3.detect_planes(c, 0xFFF, 1, 3, 1, 10, workspace=ws))
+    flags, _ = d3.detect_planes(c, 0xFFF, 1, 3, 1, 10, workspace=ws)
+    yield {"config": "detect-N128", "transform": "drt+detect_planes", "N": N, "dodecants": 12,
+           "forward_ms": t_fwd, "detect_ms": t_det, "coef_gbs_detect": c.numel() * 4 / (t_det * 1e-3) / 1e9,
+           "planes_found": int(flags.sum())}
+    N = 64
+    g = torch.from_numpy(rng.integers(0, 201, (N, N, N)).astype(np.int32)).cuda()
+    lc = d3.lines(g, 0x001)
+    kept = torch.empty_like(lc)
+
+    def pipe():
+        d3.lines(g, 0x001, out=lc)
+        d3.coef_threshold(lc, 95, 100, out=kept, workspace=ws)
+        d3.lines_adjoint(kept, 0x001)
+    t_pipe = _time(pipe)
+    t_thr = _time(lambda: d3.coef_threshold(lc, 95, 100, out=kept, workspace=ws))
+    yield {"config": "denoise-N64", "transform": "djt+threshold+djt_adjoint", "N": N, "dodecants": 1,
+           "pipeline_ms": t_pipe, "threshold_ms": t_thr, "coef_gbs_threshold": 2 * lc.numel() * 4 / (t_thr * 1e-3) / 1e9}
+
+
 if __name__ == "__main__":
     cfgs = [int(a) for a in sys.argv[1:]] or [1, 2, 3, 4, 5]
     for c in cfgs:
@@ -132,3 +182,5 @@ if __name__ == "__main__":
             print(json.dumps(run_adjoint(c)), flush=True)
         for n in (64, 128, 256):
             print(json.dumps(run_invert(n)), flush=True)
+        for r in run_apps():
+            print(json.dumps(r), flush=True)
