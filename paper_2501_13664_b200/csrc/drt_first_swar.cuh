@@ -71,6 +71,17 @@ __device__ unsigned long long d3_swar_prof[16];
 #define SW_MARK(i)
 #endif
 
+// Output staging rows (r1, r2) start row_skew(r1) = r1 words after their 33-word slot: the
+// unpack writes of a warp cover 4 consecutive r1 whose slots are 16 rows = 528 words apart
+// (0 mod 16 banks); with the skew the r1 blocks are 529 = 17 (mod 32) words apart, so the four
+// land on distinct residues mod 4 and the stores are conflict-free.  Rows never overlap (the
+// skew grows by one word per 16-row block); the copy-out reads collide on one lane pair at most.
+#ifdef D3_SWAR_NO_SKEW
+__device__ __forceinline__ int row_skew(int) { return 0; }
+#else
+__device__ __forceinline__ int row_skew(int r1) { return r1; }
+#endif
+
 #ifndef SWAR_FMA16
 #define SWAR_FMA16 0                                      // all adds IADD3 (measured fastest)
 #endif
@@ -280,7 +291,8 @@ drt_first_swar_kernel(const DrtPass p) {
                     const uint32_t sel = h ? 0x7632u : 0x5410u;
 #pragma unroll
                     for (int r2 = 0; r2 < S; ++r2) {
-                        uint32_t *o = reinterpret_cast<uint32_t *>(sm + G::ORP * ((grp + h * H2) * S + r2)) + (R / 2) * run;
+                        uint32_t *o = reinterpret_cast<uint32_t *>(sm + G::ORP * ((grp + h * H2) * S + r2)) +
+                                      row_skew(grp + h * H2) + (R / 2) * run;
 #pragma unroll
                         for (int i = 0; i < R / 2; ++i) o[i] = __byte_perm(acc[r2][2 * i], acc[r2][2 * i + 1], sel);
                     }
@@ -310,11 +322,23 @@ drt_first_swar_kernel(const DrtPass p) {
         const int rho = (r1 * wv1 + r2 * wv2) & 7;
         const long long row = ((((long long)r1 << K) + r2) << (2 * m)) + ((long long)V1 << m) + V2;
         uint16_t *dst = outp + out_inst + row * p.out_pitch + d0;
-        const uint32_t *srow = reinterpret_cast<const uint32_t *>(sm + G::ORP * rr) + (rho >> 1);
         const uint32_t sel = (rho & 1) ? 0x5432u : 0x3210u;
-        uint32_t w[4 * NCK + 1];                          // the row's words, loaded before any store
+        uint32_t w[4 * NCK + 1];                          // the row's words from rho/2, loaded before any store
+        {
+            // every lane reads its row from word 0 (odd row pitch: conflict-free), the rho/2 word
+            // offset is applied with selects (overruns the row by 3 words: inside the staging area)
+            const uint32_t *srow = reinterpret_cast<const uint32_t *>(sm + G::ORP * rr) + row_skew(r1);
+            static_assert(G::SMEM0 >= S * S * G::ORP + 4 * S + 12, "skewed rows + copy-out overrun");
+            uint32_t w0[4 * NCK + 4];
 #pragma unroll
-        for (int i = 0; i < 4 * NCK + 1; ++i) w[i] = srow[i];
+            for (int i = 0; i < 4 * NCK + 4; ++i) w0[i] = srow[i];
+            const int q = rho >> 1;
+#pragma unroll
+            for (int i = 0; i < 4 * NCK + 1; ++i) {
+                const uint32_t c4[4] = {w0[i], w0[i + 1], w0[i + 2], w0[i + 3]};
+                w[i] = sel4(c4, q);
+            }
+        }
 #pragma unroll
         for (int k = 0; k < NCK; ++k) {
             uint32_t v[4];
@@ -331,7 +355,7 @@ drt_first_swar_kernel(const DrtPass p) {
         }
         if (rho > 0 && d0 >= 8) {
             // tile elements [0, rho) end the previous chunk: window (zeros, row words 0..3)
-            const uint32_t *r0 = reinterpret_cast<const uint32_t *>(sm + G::ORP * rr);
+            const uint32_t *r0 = reinterpret_cast<const uint32_t *>(sm + G::ORP * rr) + row_skew(r1);
             uint32_t tw[8] = {0u, 0u, 0u, 0u, r0[0], r0[1], r0[2], r0[3]}, v[4];
             window_chunk<2>(tw, rho, 0, v);
             store_chunk_tail<2>(dst - 8, v, rho);
