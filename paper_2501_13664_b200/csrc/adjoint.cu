@@ -15,6 +15,7 @@
 #include <cstdlib>
 
 #include "adjoint.h"
+#include "adjoint_pass.cuh"
 
 namespace d3 {
 
@@ -225,17 +226,65 @@ __device__ __forceinline__ int orient(const int (&c)[3], int p, int N) {
     return p > 0 ? v : N - 1 - v;
 }
 
+// b0: level-0 rows (x', y') with pitch `pitch`, z' at element off + z'
 template <class T>
 __global__ void drt_adj_scatter(const T *__restrict__ b0, T *__restrict__ cube, int N, int p0, int p1, int p2,
-                                bool first) {
+                                bool first, int pitch, int off) {
     const int c2 = blockIdx.y * blockDim.x + threadIdx.x;
     if (c2 >= N) return;
     const int c0 = blockIdx.x / N;
     const int c[3] = {c0, (int)blockIdx.x - c0 * N, c2};
     const int x = orient(c, p0, N), y = orient(c, p1, N), z = orient(c, p2, N);
-    const T v = b0[((size_t)x * N + y) * (3 * N) + 2 * N + z];
+    const T v = b0[((size_t)x * N + y) * pitch + off + z];
     const size_t idx = (size_t)blockIdx.x * N + c2;
     cube[idx] = first ? v : cube[idx] + v;
+}
+
+// Transposing variant for orientations whose z' is not the cube's fast axis c2: a 32 x 32 tile of
+// the (c_az, c2) plane (c_az = the cube axis carrying z') goes through shared memory so that the
+// b0 reads run along z' and the cube read-modify-writes along c2.  grid (N/32 c2 tiles,
+// N/32 c_az tiles, N values of the third axis), block 32 x 8.
+template <class T>
+__global__ void drt_adj_scatter_t(const T *__restrict__ b0, T *__restrict__ cube, int N, int p0, int p1, int p2,
+                                  bool first, int pitch, int off) {
+    __shared__ T tile[32][33];
+    const int az = (p2 < 0 ? -p2 : p2) - 1;                         // 0 or 1 here
+    const int ao = 1 - az;                                           // the remaining axis
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int c2b = blockIdx.x * 32, czb = blockIdx.y * 32, co = blockIdx.z;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        int c[3];
+        c[2] = c2b + ty + 8 * i;
+        c[az] = czb + tx;
+        c[ao] = co;
+        const int x = orient(c, p0, N), y = orient(c, p1, N), z = orient(c, p2, N);
+        tile[ty + 8 * i][tx] = b0[((size_t)x * N + y) * pitch + off + z];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        int c[3];
+        c[2] = c2b + tx;
+        c[az] = czb + ty + 8 * i;
+        c[ao] = co;
+        const size_t idx = ((size_t)c[0] * N + c[1]) * N + c[2];
+        const T v = tile[tx][ty + 8 * i];
+        cube[idx] = first ? v : cube[idx] + v;
+    }
+}
+
+template <class T>
+void drt_scatter(const T *b0, T *cube, int N, const int8_t *row, bool first, int pitch, int off, cudaStream_t st) {
+    const int p2 = row[2];
+    if ((p2 == 3 || p2 == -3) || N < 32) {
+        const unsigned t = N >= 256 ? 256u : (unsigned)((N + 31) / 32 * 32);
+        drt_adj_scatter<T><<<dim3((unsigned)(N * N), (unsigned)((N + t - 1) / t)), t, 0, st>>>(b0, cube, N, row[0], row[1],
+                                                                                              p2, first, pitch, off);
+    } else {
+        drt_adj_scatter_t<T><<<dim3((unsigned)(N / 32), (unsigned)(N / 32), (unsigned)N), dim3(32, 8), 0, st>>>(
+            b0, cube, N, row[0], row[1], p2, first, pitch, off);
+    }
 }
 
 // ---- DJT stage m: rows i = vm + 2 v + 2^(n-m) sg1 + 2^n sg2, (D1, D2) in [0, 2N)^2:
@@ -377,6 +426,102 @@ void djt_stage(int L, const T *in, T *out, int N, int n, int m_lo, bool from_coe
 }
 }  // namespace
 
+// ---- DRT backprojection by radix-2^K pass kernels (adjoint_pass.cuh): the forward's pass plan
+// run backwards, levels n -> ... -> 0, then the seeding / orientation transpose.
+namespace {
+struct Level {
+    int base, pitch;
+};
+// Level c storage: E = base + p.  For an intermediate level the base is chosen below lo_c so that
+// the tile grid of the pass that READS it (its first tile at e = `ebase_reader`, staged from
+// e - 2H) starts on a 4-element chunk: no tile is spent on a few misaligned columns.
+inline Level level_layout(int N, int n, int c, int ebase_reader = 0, int h_reader = 0) {
+    if (c == n) return {0, 3 * N};                                   // the caller's coefficients
+    if (c == 0) return {2 * N, (N + 3) / 4 * 4};                     // z' = E - 2N
+    const int lo = 2 * N - 2 * ((1 << c) - 1);
+    int base = lo;
+    base -= (((ebase_reader - 2 * h_reader - base) % 4) + 4) % 4;
+    return {base, (3 * N - base + 15) / 16 * 16};
+}
+// lowest needed E of level c, and the first tile's e for the pass that writes level c with radix K
+inline int level_lo(int N, int c) { return c == 0 ? 2 * N : 2 * N - 2 * ((1 << c) - 1); }
+inline int pass_ebase(int N, int c, int K) { return level_lo(N, c) - 2 * ((1 << K) - 1) * ((1 << c) - 1); }
+inline int pass_plan(int n, int (&ks)[4]) {                          // forward order, first pass first
+    const int np = (n + 3) / 4;
+    for (int i = 0; i < np; ++i) ks[i] = n / np + (i < n % np ? 1 : 0);
+    return np;
+}
+
+constexpr int kAdjT = 64, kAdjR = 8;
+
+template <int K, class T>
+void launch_adj_pass(const AdjPass &a, int ntiles, int groups, cudaStream_t st) {
+    using G = DrtGeom<K, kAdjR, kAdjT, false>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(drt_adj_pass_kernel<K, kAdjR, kAdjT, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(drt_adj_pass_kernel<K, kAdjR, kAdjT, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             G::SMEM);
+        attr = true;
+    }
+    drt_adj_pass_kernel<K, kAdjR, kAdjT, T><<<dim3((unsigned)ntiles, (unsigned)groups, 1), G::THREADS, G::SMEM, st>>>(a);
+}
+
+bool adj_use_passes(int N) {
+    static const bool off = getenv("D3_ADJ_MODE") && *getenv("D3_ADJ_MODE");   // set: the stage kernels
+    return !off && N >= 4;
+}
+
+// one instance: coefficients `src` (level n) -> level-0 rows in `l0`; returns launches
+template <class T>
+int drt_adj_passes(const T *src, int N, int n, T *tmp0, T *tmp1, T *l0, cudaStream_t st) {
+    int ks[4];
+    const int np = pass_plan(n, ks);
+    int c_hi = n, nl = 0;
+    const T *in = src;
+    T *bufs[2] = {tmp0, tmp1};
+    for (int i = np - 1; i >= 0; --i) {
+        const int K = ks[i], c = c_hi - K;
+        const int eb = pass_ebase(N, c, K), H = (1 << K) - 1;
+        // this pass reads level c_hi (written by the previous pass with this pass's tile grid) and
+        // writes level c (read by the next pass, radix ks[i - 1])
+        const Level li = level_layout(N, n, c_hi, eb, H);
+        const Level lo = c > 0 ? level_layout(N, n, c, pass_ebase(N, c - ks[i - 1], ks[i - 1]), (1 << ks[i - 1]) - 1)
+                               : level_layout(N, n, 0);
+        T *out = c == 0 ? l0 : bufs[i & 1];
+        AdjPass a{};
+        a.in = in;
+        a.out = out;
+        a.N = N;
+        a.n = n;
+        a.c = c;
+        a.m = n - c - K;
+        a.in_pitch = li.pitch;
+        a.in_base = li.base;
+        a.in_width = li.pitch;
+        a.out_pitch = lo.pitch;
+        a.out_base = lo.base;
+        a.out_width = lo.pitch;
+        a.lo = level_lo(N, c);
+        a.ebase = eb;
+        if ((((eb - 2 * H - li.base) % 4) + 4) % 4 != 0) a.ebase -= (((eb - 2 * H - li.base) % 4) + 4) % 4;   // coefficients: base 0
+        a.one = 1u;
+        const int ntiles = (3 * N - a.ebase + kAdjT - 1) / kAdjT;
+        const int groups = 1 << (2 * (n - K));
+        switch (K) {
+            case 1: launch_adj_pass<1, T>(a, ntiles, groups, st); break;
+            case 2: launch_adj_pass<2, T>(a, ntiles, groups, st); break;
+            case 3: launch_adj_pass<3, T>(a, ntiles, groups, st); break;
+            default: launch_adj_pass<4, T>(a, ntiles, groups, st); break;
+        }
+        ++nl;
+        in = out;
+        c_hi = c;
+    }
+    return nl;
+}
+}  // namespace
+
 template <class T>
 static drt3d_status run_adj(int transform, const void *coef, int N, int n, const int8_t (*rows)[3], uint32_t mask,
                             int batch, void *cube, void *ws, cudaStream_t st, int *launches) {
@@ -396,6 +541,17 @@ static drt3d_status run_adj(int transform, const void *coef, int N, int n, const
         for (int k = 0; k < 12; ++k) {
             if (!((mask >> k) & 1)) continue;
             const T *src = cf + ((long long)b * K + j) * cells;
+            if (transform == 0 && adj_use_passes(N)) {
+                // level-0 rows go to buf[1] (N^2 x N), intermediates alternate buf[0] / the upper
+                // part of buf[1] (a level-c buffer is at most N^2 x 2N here; n > 8 needs two)
+                T *l0 = buf[1];
+                T *t1 = buf[1] + (long long)N * N * ((N + 3) / 4 * 4);
+                nl += drt_adj_passes<T>(src, N, n, buf[0], t1, l0, st);
+                drt_scatter<T>(l0, cb + (long long)b * n3, N, rows[k], j == 0, (N + 3) / 4 * 4, 0, st);
+                ++nl;
+                ++j;
+                continue;
+            }
             int cur = 0;
             for (int m_hi = n - 1; m_hi >= 0;) {
                 const int L = m_hi + 1 < Lmax ? m_hi + 1 : Lmax, m_lo = m_hi - L + 1;
@@ -412,7 +568,7 @@ static drt3d_status run_adj(int transform, const void *coef, int N, int n, const
             const T *b0 = buf[cur ^ 1];
             if (transform == 0)
                 drt_adj_scatter<T><<<sg, sb, 0, st>>>(b0, cb + (long long)b * n3, N, rows[k][0], rows[k][1],
-                                                      rows[k][2], j == 0);
+                                                      rows[k][2], j == 0, 3 * N, 2 * N);
             else
                 djt_adj_scatter<T><<<sg, sb, 0, st>>>(b0, cb + (long long)b * n3, N, rows[k][0], rows[k][1],
                                                       rows[k][2], j == 0);

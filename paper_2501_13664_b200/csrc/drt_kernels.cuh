@@ -121,7 +121,9 @@ __device__ __forceinline__ Acc add2(Acc acc, uint32_t x, uint32_t y, uint32_t on
 __host__ __device__ constexpr bool fma_row(int r, int fma16) { return ((r + 1) * fma16) / 16 > (r * fma16) / 16; }
 
 // FMA16 = -1: the measured default, rows with r % 4 < 1 (1/4 of the rows; swept 0 .. 3/8).
-template <int K, int R, int SP, bool U16, class Acc, int FMA16 = -1>
+// TR (transposed, the backprojection pass of adjoint_pass.cuh): output r, input a at offset
+// (S - 1) - l^K_a(r), i.e. acc[w][j] += row_r[j + H - l^K_r(w)].
+template <int K, int R, int SP, bool U16, class Acc, int FMA16 = -1, bool TR = false>
 __device__ __forceinline__ void drt_accumulate(const unsigned char *__restrict__ sm, int slot0, int sstep, int c0,
                                                uint32_t one, Acc (&acc)[1 << K][R]) {
     constexpr int S = 1 << K;
@@ -157,12 +159,15 @@ __device__ __forceinline__ void drt_accumulate(const unsigned char *__restrict__
     } else {
         static_for<0, S / 2>([&](auto p_) {
             constexpr int a0 = 2 * decltype(p_)::value, a1 = a0 + 1;
-            uint32_t b0[R + a0], b1[R + a1];
-            load(a0, R + a0, b0);
-            load(a1, R + a1, b1);
+            // forward offsets l^K_r(a) <= a; transposed ones (S - 1) - l^K_a(r) reach S - 1
+            constexpr int n0 = R + (TR ? S - 1 : a0), n1 = R + (TR ? S - 1 : a1);
+            uint32_t b0[n0], b1[n1];
+            load(a0, n0, b0);
+            load(a1, n1, b1);
             static_for<0, S>([&](auto r_) {
                 constexpr int r = decltype(r_)::value;
-                constexpr int o0 = lk(K, r, a0), o1 = lk(K, r, a1);
+                constexpr int o0 = TR ? (S - 1) - lk(K, a0, r) : lk(K, r, a0);
+                constexpr int o1 = TR ? (S - 1) - lk(K, a1, r) : lk(K, r, a1);
 #ifndef D3_FMA_MOD
 #define D3_FMA_MOD 4
 #define D3_FMA_LT 1
