@@ -125,7 +125,9 @@ drt3d_status djt3d_lines(const void *cube, int N, uint32_t dodecant_mask, void *
  * planes, [batch][K][N][N][2N][2N] for lines) with element type opts->out_dtype
  * (I32: exact sums mod 2^32; F32: fp32 accumulation); cube: [batch][N][N][N]
  * of the same element type (opts->in_dtype is ignored).  STACKED layout only.
- * Workspace: two stage buffers (query the size).                              */
+ * Workspace: query the size (it depends on N and on the number of dodecants:
+ * the DRT runs the dodecants of a chunk together, up to 4 GB of level
+ * buffers -- all 12 at N = 256, 1.7 GB).                                     */
 drt3d_status drt3d_planes_adjoint_workspace_size(int N, uint32_t dodecant_mask, const drt3d_opts *opts,
                                                  size_t *bytes);
 drt3d_status drt3d_planes_adjoint(const void *coef, int N, uint32_t dodecant_mask, void *cube,

@@ -287,6 +287,67 @@ void drt_scatter(const T *b0, T *cube, int N, const int8_t *row, bool first, int
     }
 }
 
+// All dodecants of a chunk at once: cube[c] (=|+=) sum_j l0_j[orient_j(c)] in the fixed order j
+// (deterministic).  A CTA owns an 8 (c0) x 8 (c1) x 32 (c2) tile; for every dodecant the matching
+// box of its level-0 rows is read along z' (runs of 8 or 32 elements: whole 32-byte sectors) into
+// shared memory in cube order, then added to the CTA's registers; one coalesced write at the end.
+constexpr int kGatherMax = 12;
+struct GatherArgs {
+    int D;                               // dodecants in this chunk
+    int8_t rows[kGatherMax][3];
+};
+template <class T>
+__global__ void __launch_bounds__(256) drt_adj_gather(const T *__restrict__ l0, long long l0_stride, int pitch, int N,
+                                                      const GatherArgs g, T *__restrict__ cube, bool first) {
+    __shared__ T sm[8 * 8 * 33];                                      // [c0 8][c1 8][c2 32 + 1 pad]
+    const int tid = threadIdx.x;
+    const int T0 = (int)blockIdx.z * 8, T1 = (int)blockIdx.y * 8, T2 = (int)blockIdx.x * 32;
+    // per cube axis a: tile origin, extent (log2) and shared-memory stride; scalar selects only
+    // (runtime-indexed arrays would go to local memory)
+    auto org = [&](int a) { return a == 0 ? T0 : (a == 1 ? T1 : T2); };
+    auto lex = [&](int a) { return a == 2 ? 5 : 3; };
+    auto str = [&](int a) { return a == 0 ? 8 * 33 : (a == 1 ? 33 : 1); };
+    T acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = T(0);
+    for (int j = 0; j < g.D; ++j) {
+        const int p0 = g.rows[j][0], p1 = g.rows[j][1], p2 = g.rows[j][2];
+        const int a0 = (p0 < 0 ? -p0 : p0) - 1, a1 = (p1 < 0 ? -p1 : p1) - 1, a2 = (p2 < 0 ? -p2 : p2) - 1;
+        const int l0e = lex(a0), l1e = lex(a1), l2e = lex(a2);
+        // lowest oriented coordinate of the box along x', y', z'
+        const int o0 = p0 > 0 ? org(a0) : N - org(a0) - (1 << l0e);
+        const int o1 = p1 > 0 ? org(a1) : N - org(a1) - (1 << l1e);
+        const int o2 = p2 > 0 ? org(a2) : N - org(a2) - (1 << l2e);
+        // shared index of oriented offset (xo, yo, zo): base + xo m0 + yo m1 + zo m2
+        const int m0 = p0 > 0 ? str(a0) : -str(a0), m1 = p1 > 0 ? str(a1) : -str(a1), m2 = p2 > 0 ? str(a2) : -str(a2);
+        const int base = (p0 > 0 ? 0 : ((1 << l0e) - 1) * str(a0)) + (p1 > 0 ? 0 : ((1 << l1e) - 1) * str(a1)) +
+                         (p2 > 0 ? 0 : ((1 << l2e) - 1) * str(a2));
+        const T *src = l0 + (long long)j * l0_stride + ((size_t)o0 * N + o1) * pitch + o2;
+        T v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int e = tid + 256 * i;
+            const int zo = e & ((1 << l2e) - 1), yo = (e >> l2e) & ((1 << l1e) - 1), xo = e >> (l2e + l1e);
+            v[i] = __ldg(src + ((size_t)xo * N + yo) * pitch + zo);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int e = tid + 256 * i;
+            const int zo = e & ((1 << l2e) - 1), yo = (e >> l2e) & ((1 << l1e) - 1), xo = e >> (l2e + l1e);
+            sm[base + xo * m0 + yo * m1 + zo * m2] = v[i];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = acc[i] + sm[(i * 8 + (tid >> 5)) * 33 + (tid & 31)];
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const size_t idx = ((size_t)(T0 + i) * N + T1 + (tid >> 5)) * N + T2 + (tid & 31);
+        cube[idx] = first ? acc[i] : cube[idx] + acc[i];
+    }
+}
+
 // ---- DJT stage m: rows i = vm + 2 v + 2^(n-m) sg1 + 2^n sg2, (D1, D2) in [0, 2N)^2:
 //   b^m(i, d1, d2) = sum_{b1,b2} b^{m+1}(v + 2^(n-m-1) b1 + 2^(n-m) sg1 + 2^n b2 + 2^(n+1) sg2,
 //                                        d1 - vm (b1 + sg1), d2 - vm (b2 + sg2)).
@@ -455,7 +516,7 @@ inline int pass_plan(int n, int (&ks)[4]) {                          // forward 
 constexpr int kAdjT = 64, kAdjR = 8;
 
 template <int K, class T>
-void launch_adj_pass(const AdjPass &a, int ntiles, int groups, cudaStream_t st) {
+void launch_adj_pass(const AdjPass &a, int ntiles, int groups, int D, cudaStream_t st) {
     using G = DrtGeom<K, kAdjR, kAdjT, false>;
     static bool attr = false;
     if (!attr) {
@@ -464,7 +525,37 @@ void launch_adj_pass(const AdjPass &a, int ntiles, int groups, cudaStream_t st) 
                              G::SMEM);
         attr = true;
     }
-    drt_adj_pass_kernel<K, kAdjR, kAdjT, T><<<dim3((unsigned)ntiles, (unsigned)groups, 1), G::THREADS, G::SMEM, st>>>(a);
+    drt_adj_pass_kernel<K, kAdjR, kAdjT, T><<<dim3((unsigned)ntiles, (unsigned)groups, (unsigned)D), G::THREADS, G::SMEM,
+                                               st>>>(a);
+}
+
+// Pass-path workspace for a chunk of D dodecants: level-0 rows (D x N^2 x P0) and two
+// intermediate regions (D x N^2 x the widest intermediate pitch); chunks are sized so the
+// workspace stays within kAdjBudget (all 12 dodecants up to N = 256).
+constexpr size_t kAdjBudget = 4ull << 30;
+struct AdjWs {
+    long long l0_stride, mid_stride;     // elements per dodecant
+    int D;                               // dodecants per chunk
+    size_t bytes;
+};
+inline AdjWs adj_ws(int N, int n, int K) {
+    int ks[4];
+    const int np = pass_plan(n, ks);
+    int maxp = 0, c = 0;
+    for (int i = 0; i < np - 1; ++i) {                               // intermediate levels c = ks[0], ks[0]+ks[1], ..
+        c += ks[i];
+        const Level l = level_layout(N, n, c, 0, 0);
+        maxp = l.pitch + 16 > maxp ? l.pitch + 16 : maxp;            // + slack for the reader-aligned base
+    }
+    AdjWs w;
+    w.l0_stride = (long long)N * N * ((N + 3) / 4 * 4);
+    w.mid_stride = (long long)N * N * maxp;
+    const size_t per = (size_t)(w.l0_stride + (np > 2 ? 2 : 1) * w.mid_stride) * 4;
+    const size_t fit = kAdjBudget / (per ? per : 1);
+    w.D = K < (int)(fit ? fit : 1) ? K : (int)(fit ? fit : 1);
+    if (w.D > kGatherMax) w.D = kGatherMax;
+    w.bytes = (per * (size_t)w.D + 255) / 256 * 256;
+    return w;
 }
 
 bool adj_use_passes(int N) {
@@ -474,7 +565,7 @@ bool adj_use_passes(int N) {
 
 // one instance: coefficients `src` (level n) -> level-0 rows in `l0`; returns launches
 template <class T>
-int drt_adj_passes(const T *src, int N, int n, T *tmp0, T *tmp1, T *l0, cudaStream_t st) {
+int drt_adj_passes(const T *src, int N, int n, int D, const AdjWs &w, T *tmp0, T *tmp1, T *l0, cudaStream_t st) {
     int ks[4];
     const int np = pass_plan(n, ks);
     int c_hi = n, nl = 0;
@@ -499,6 +590,8 @@ int drt_adj_passes(const T *src, int N, int n, T *tmp0, T *tmp1, T *l0, cudaStre
         a.in_pitch = li.pitch;
         a.in_base = li.base;
         a.in_width = li.pitch;
+        a.in_inst_stride = c_hi == n ? (long long)N * N * 3 * N : w.mid_stride;
+        a.out_inst_stride = c == 0 ? w.l0_stride : w.mid_stride;
         a.out_pitch = lo.pitch;
         a.out_base = lo.base;
         a.out_width = lo.pitch;
@@ -509,10 +602,10 @@ int drt_adj_passes(const T *src, int N, int n, T *tmp0, T *tmp1, T *l0, cudaStre
         const int ntiles = (3 * N - a.ebase + kAdjT - 1) / kAdjT;
         const int groups = 1 << (2 * (n - K));
         switch (K) {
-            case 1: launch_adj_pass<1, T>(a, ntiles, groups, st); break;
-            case 2: launch_adj_pass<2, T>(a, ntiles, groups, st); break;
-            case 3: launch_adj_pass<3, T>(a, ntiles, groups, st); break;
-            default: launch_adj_pass<4, T>(a, ntiles, groups, st); break;
+            case 1: launch_adj_pass<1, T>(a, ntiles, groups, D, st); break;
+            case 2: launch_adj_pass<2, T>(a, ntiles, groups, D, st); break;
+            case 3: launch_adj_pass<3, T>(a, ntiles, groups, D, st); break;
+            default: launch_adj_pass<4, T>(a, ntiles, groups, D, st); break;
         }
         ++nl;
         in = out;
@@ -536,22 +629,48 @@ static drt3d_status run_adj(int transform, const void *coef, int N, int n, const
     const int Lmax = Lb > 0 ? Lb : adj_fuse();
     const dim3 sg((unsigned)(N * N), chunks(N)), sb(tpb(N));
     int nl = 0;
+    if (transform == 0 && adj_use_passes(N)) {
+        // pass kernels over chunks of D dodecants, then one gather into the cube per chunk
+        const AdjWs w = adj_ws(N, n, K);
+        int ks[4];
+        const int np = pass_plan(n, ks);
+        T *l0 = reinterpret_cast<T *>(ws);
+        T *mid0 = l0 + (long long)w.D * w.l0_stride;
+        T *mid1 = np > 2 ? mid0 + (long long)w.D * w.mid_stride : mid0;
+        int kl[12], nk = 0;
+        for (int k = 0; k < 12; ++k)
+            if ((mask >> k) & 1) kl[nk++] = k;
+        const int P0 = (N + 3) / 4 * 4;
+        for (int b = 0; b < batch; ++b) {
+            T *cube_b = cb + (long long)b * n3;
+            for (int j0 = 0; j0 < K; j0 += w.D) {
+                const int d = K - j0 < w.D ? K - j0 : w.D;
+                nl += drt_adj_passes<T>(cf + ((long long)b * K + j0) * cells, N, n, d, w, mid0, mid1, l0, st);
+                if (N >= 32) {
+                    GatherArgs g{};
+                    g.D = d;
+                    for (int jj = 0; jj < d; ++jj)
+                        for (int t = 0; t < 3; ++t) g.rows[jj][t] = rows[kl[j0 + jj]][t];
+                    drt_adj_gather<T><<<dim3((unsigned)(N / 32), (unsigned)(N / 8), (unsigned)(N / 8)), 256, 0, st>>>(
+                        l0, w.l0_stride, P0, N, g, cube_b, j0 == 0);
+                    ++nl;
+                } else {
+                    for (int jj = 0; jj < d; ++jj) {
+                        drt_scatter<T>(l0 + (long long)jj * w.l0_stride, cube_b, N, rows[kl[j0 + jj]], j0 + jj == 0, P0, 0,
+                                       st);
+                        ++nl;
+                    }
+                }
+            }
+        }
+        if (launches) *launches = nl;
+        return cudaGetLastError() == cudaSuccess ? DRT3D_OK : DRT3D_ERR_CUDA;
+    }
     for (int b = 0; b < batch; ++b) {
         int j = 0;
         for (int k = 0; k < 12; ++k) {
             if (!((mask >> k) & 1)) continue;
             const T *src = cf + ((long long)b * K + j) * cells;
-            if (transform == 0 && adj_use_passes(N)) {
-                // level-0 rows go to buf[1] (N^2 x N), intermediates alternate buf[0] / the upper
-                // part of buf[1] (a level-c buffer is at most N^2 x 2N here; n > 8 needs two)
-                T *l0 = buf[1];
-                T *t1 = buf[1] + (long long)N * N * ((N + 3) / 4 * 4);
-                nl += drt_adj_passes<T>(src, N, n, buf[0], t1, l0, st);
-                drt_scatter<T>(l0, cb + (long long)b * n3, N, rows[k], j == 0, (N + 3) / 4 * 4, 0, st);
-                ++nl;
-                ++j;
-                continue;
-            }
             int cur = 0;
             for (int m_hi = n - 1; m_hi >= 0;) {
                 const int L = m_hi + 1 < Lmax ? m_hi + 1 : Lmax, m_lo = m_hi - L + 1;
@@ -580,10 +699,17 @@ static drt3d_status run_adj(int transform, const void *coef, int N, int n, const
     return cudaGetLastError() == cudaSuccess ? DRT3D_OK : DRT3D_ERR_CUDA;
 }
 
-size_t adjoint_workspace_bytes(int transform, int N) {
+size_t adjoint_workspace_bytes(int transform, int N, uint32_t mask) {
     const long long W = transform == 0 ? 3LL * N : 2LL * N;
     const long long cells = transform == 0 ? (long long)N * N * W : (long long)N * N * W * W;
-    return (size_t)(2 * cells * 4 + 255) / 256 * 256;
+    size_t b = (size_t)(2 * cells * 4 + 255) / 256 * 256;            // the stage kernels' two buffers
+    if (transform == 0 && N >= 4) {                                  // the pass path (default)
+        int n = 0;
+        while ((1 << n) < N) ++n;
+        const size_t pb = adj_ws(N, n, __builtin_popcount(mask & 0xFFFu)).bytes;
+        b = pb > b ? pb : b;
+    }
+    return b;
 }
 
 drt3d_status run_adjoint(int transform, const void *coef, int N, int n, const int8_t (*rows)[3], uint32_t mask,

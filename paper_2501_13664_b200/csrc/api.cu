@@ -580,7 +580,7 @@ static drt3d_status adjoint_ws(int transform, int N, uint32_t mask, const drt3d_
     int n;
     drt3d_status s = adjoint_check(transform, N, mask, o, n);
     if (s != DRT3D_OK) return s;
-    *bytes = d3::adjoint_workspace_bytes(transform, N);
+    *bytes = d3::adjoint_workspace_bytes(transform, N, mask);
     return DRT3D_OK;
 }
 
@@ -592,7 +592,7 @@ static drt3d_status adjoint_run(int transform, const void *coef, int N, uint32_t
     drt3d_status s = adjoint_check(transform, N, mask, o, n);
     if (s != DRT3D_OK) return s;
     if (!coef || !cube) return DRT3D_ERR_INVALID_ARG;
-    if (!ws || ws_bytes < d3::adjoint_workspace_bytes(transform, N)) return DRT3D_ERR_WORKSPACE;
+    if (!ws || ws_bytes < d3::adjoint_workspace_bytes(transform, N, mask)) return DRT3D_ERR_WORKSPACE;
     const int K = popcount12(mask);
     const size_t cb = (size_t)o.batch * N * N * N * 4;
     const size_t ob = (size_t)o.batch * K * N * N * (transform == 0 ? 3 * N : 4 * N * N) * 4;
