@@ -154,7 +154,7 @@ drt3d_status djt3d_lines_adjoint(const void *coef, int N, uint32_t dodecant_mask
  * fp32 device, receives x_iters; rnorm: NULL or a device array of iters+1
  * doubles receiving ||b - A x_k||_2, k = 0..iters.
  * opts: NULL or batch = 1, out_dtype = F32, STACKED (in_dtype ignored).
- * Workspace: per level n = N, N/2, .., n_min four coefficient-sized and three
+ * Workspace: per level n = N, N/2, .., n_min three coefficient-sized and three
  * cube-sized fp32 buffers, plus the larger of the size-N forward / adjoint
  * workspaces (query the size; 256-byte aligned).
  * Enqueue only: every iteration runs on `stream` with no host synchronisation

@@ -22,7 +22,7 @@
 namespace d3 {
 namespace inv {
 
-constexpr int kRedBlocks = 592;      // 4 x 148 SMs, fixed so the reduction order is fixed
+constexpr int kRedBlocks = 1184;     // 8 x 148 SMs, fixed so the reduction order is fixed
 constexpr int kRedThreads = 256;
 
 __device__ __forceinline__ double block_sum(double v, double *sh) {
@@ -40,15 +40,18 @@ __device__ __forceinline__ double block_sum(double v, double *sh) {
     return t;                                   // valid in thread 0
 }
 
-// part[2 blk] = sum r*q, part[2 blk + 1] = sum q*q over this block's grid-stride share
+// part[2 blk] = sum r*q, part[2 blk + 1] = sum q*q over this block's grid-stride share.
+// Element counts of the coefficient and cube arrays are multiples of 4 (N >= 2) and every
+// buffer is 256-byte aligned: the streaming kernels use 16-byte accesses.
 __global__ void __launch_bounds__(kRedThreads) dot_rq_qq(const float *__restrict__ r, const float *__restrict__ q,
                                                           size_t n, double *__restrict__ part) {
     __shared__ double sh[2][kRedThreads / 32];
     double rq = 0.0, qq = 0.0;
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        const double a = r[i], b = q[i];
-        rq += a * b;
-        qq += b * b;
+    const float4 *r4 = reinterpret_cast<const float4 *>(r), *q4 = reinterpret_cast<const float4 *>(q);
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n / 4; i += (size_t)gridDim.x * blockDim.x) {
+        const float4 a = r4[i], b = q4[i];
+        rq += (double)a.x * b.x + (double)a.y * b.y + (double)a.z * b.z + (double)a.w * b.w;
+        qq += (double)b.x * b.x + (double)b.y * b.y + (double)b.z * b.z + (double)b.w * b.w;
     }
     const double s0 = block_sum(rq, sh[0]);
     const double s1 = block_sum(qq, sh[1]);
@@ -58,7 +61,6 @@ __global__ void __launch_bounds__(kRedThreads) dot_rq_qq(const float *__restrict
     }
 }
 
-// alpha = (sum rq) / (sum qq), 0 when A p = 0
 __global__ void finalize_alpha(const double *__restrict__ part, int nb, double *__restrict__ alpha) {
     __shared__ double sh[2][kRedThreads / 32];
     double rq = 0.0, qq = 0.0;
@@ -71,16 +73,20 @@ __global__ void finalize_alpha(const double *__restrict__ part, int nb, double *
     if (threadIdx.x == 0) *alpha = s1 > 0.0 ? s0 / s1 : 0.0;
 }
 
-// r <- r - alpha q (fp32), part[blk] = sum r_new^2
-__global__ void __launch_bounds__(kRedThreads) update_r(float *__restrict__ r, const float *__restrict__ q, size_t n,
-                                                         const double *__restrict__ alpha, double *__restrict__ part) {
+// dst <- src - alpha q (fp32; dst may be src), part[blk] = sum dst^2
+__global__ void __launch_bounds__(kRedThreads) update_r(const float *src, const float *__restrict__ q, float *dst,
+                                                         size_t n, const double *__restrict__ alpha,
+                                                         double *__restrict__ part) {
     __shared__ double sh[kRedThreads / 32];
     const float a = (float)*alpha;
     double rr = 0.0;
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        const float v = r[i] - a * q[i];
-        r[i] = v;
-        rr += (double)v * v;
+    const float4 *s4 = reinterpret_cast<const float4 *>(src), *q4 = reinterpret_cast<const float4 *>(q);
+    float4 *d4 = reinterpret_cast<float4 *>(dst);
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n / 4; i += (size_t)gridDim.x * blockDim.x) {
+        const float4 u = s4[i], w = q4[i];
+        const float4 v = make_float4(u.x - a * w.x, u.y - a * w.y, u.z - a * w.z, u.w - a * w.w);
+        d4[i] = v;
+        rr += (double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z + (double)v.w * v.w;
     }
     const double s = block_sum(rr, sh);
     if (threadIdx.x == 0) part[blockIdx.x] = s;
@@ -90,9 +96,10 @@ __global__ void __launch_bounds__(kRedThreads) update_r(float *__restrict__ r, c
 __global__ void __launch_bounds__(kRedThreads) sum_sq(const float *__restrict__ r, size_t n, double *__restrict__ part) {
     __shared__ double sh[kRedThreads / 32];
     double rr = 0.0;
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        const double v = r[i];
-        rr += v * v;
+    const float4 *r4 = reinterpret_cast<const float4 *>(r);
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n / 4; i += (size_t)gridDim.x * blockDim.x) {
+        const float4 v = r4[i];
+        rr += (double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z + (double)v.w * v.w;
     }
     const double s = block_sum(rr, sh);
     if (threadIdx.x == 0) part[blockIdx.x] = s;
@@ -110,8 +117,12 @@ __global__ void finalize_norm(const double *__restrict__ part, int nb, double *_
 __global__ void update_x(float *__restrict__ x, const float *__restrict__ p, size_t n,
                          const double *__restrict__ alpha) {
     const float a = (float)*alpha;
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-        x[i] = x[i] + a * p[i];
+    float4 *x4 = reinterpret_cast<float4 *>(x);
+    const float4 *p4 = reinterpret_cast<const float4 *>(p);
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n / 4; i += (size_t)gridDim.x * blockDim.x) {
+        const float4 u = x4[i], v = p4[i];
+        x4[i] = make_float4(u.x + a * v.x, u.y + a * v.y, u.z + a * v.z, u.w + a * v.w);
+    }
 }
 
 // p = h * g, h of PAPER.md:576-591 (centre 7/8, faces -1/16, edges -1/32, corners -1/64), zero
@@ -159,8 +170,12 @@ __global__ void prolong_cube(const float *__restrict__ ec, float *__restrict__ e
 
 // out = a - b
 __global__ void diff(const float *__restrict__ a, const float *__restrict__ b, float *__restrict__ out, size_t n) {
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-        out[i] = a[i] - b[i];
+    const float4 *a4 = reinterpret_cast<const float4 *>(a), *b4 = reinterpret_cast<const float4 *>(b);
+    float4 *o4 = reinterpret_cast<float4 *>(out);
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n / 4; i += (size_t)gridDim.x * blockDim.x) {
+        const float4 u = a4[i], v = b4[i];
+        o4[i] = make_float4(u.x - v.x, u.y - v.y, u.z - v.z, u.w - v.w);
+    }
 }
 
 inline size_t align256(size_t b) { return (b + 255) / 256 * 256; }
@@ -168,8 +183,8 @@ inline size_t align256(size_t b) { return (b + 255) / 256 * 256; }
 constexpr int kMaxLevels = 11;
 
 // Per grid level (0 = the caller's size N, level l has size N >> l): residual r, its remainder
-// rp = r - A e, A e, A p (coefficient-sized); e, A^T rp, p (cube-sized).  Level 0's r is the
-// outer residual.
+// rp = r - A e, and A e / A p sharing one buffer (coefficient-sized); e, A^T rp, p (cube-sized).
+// Level 0's r is the outer residual.
 struct Level {
     int n;
     size_t ncoef, ncube;
@@ -210,8 +225,8 @@ inline drt3d_status layout(int N, int n_min, uint32_t mask, int table, Layout &L
         v.ncube = (size_t)n * n * n;
         v.r = off; off += align256(v.ncoef * 4);
         v.rp = off; off += align256(v.ncoef * 4);
-        v.ae = off; off += align256(v.ncoef * 4);
         v.q = off; off += align256(v.ncoef * 4);
+        v.ae = v.q;                                     // A e is dead once r' = r - A e is formed
         v.e = off; off += align256(v.ncube * 4);
         v.g = off; off += align256(v.ncube * 4);
         v.p = off; off += align256(v.ncube * 4);
@@ -291,38 +306,40 @@ drt3d_status step(Ctx &c, int l, const float *res) {
 }
 
 // Multigrid approximate inverse (R18) of the residual in level l's `r` buffer: leaves e_l = B r_l
-// in `e` and A e_l in `ae`.
+// in `e`.  A parent uses only its child's e (it applies A to the prolongated e itself), so A e_l
+// is never formed below the top; at the top (l = 0) the outer residual is updated in place,
+// r <- r' - alpha q with r' = r - A P e_c the remainder the last step minimised (r' = r on a
+// single grid), which equals r - A e_0.
 drt3d_status mg_apply(Ctx &c, int l) {
     const Level &v = c.L->lv[l];
     const unsigned nb = kRedBlocks;
-    if (l == c.L->nlev - 1) {                                    // coarsest: e = alpha p, ae = alpha q
-        drt3d_status s = step(c, l, c.f(v.r));
+    const float *rem = c.f(v.r);                                                // what the step sees
+    if (l < c.L->nlev - 1) {
+        const Level &u = c.L->lv[l + 1];
+        const int K = (int)(v.ncoef / ((size_t)v.n * v.n * 3 * v.n));
+        restrict_coef<<<(unsigned)(K * u.n * u.n), row_threads(3 * u.n), 0, c.st>>>(c.f(v.r), c.f(u.r), u.n);  // S r
+        c.nl += 1;
+        drt3d_status s = mg_apply(c, l + 1);                                                                  // B_{n/2}
         if (s != DRT3D_OK) return s;
+        prolong_cube<<<(unsigned)(v.n * v.n), row_threads(v.n), 0, c.st>>>(c.f(u.e), c.f(v.e), v.n);        // e = P e_c
+        int l1 = 0;
+        c.o.launches = &l1;
+        s = drt3d_planes(c.f(v.e), v.n, c.mask, c.f(v.ae), &c.o, c.tws(), c.L->tws_bytes, c.stream);       // A e
+        if (s != DRT3D_OK) return s;
+        diff<<<nb, kRedThreads, 0, c.st>>>(c.f(v.r), c.f(v.ae), c.f(v.rp), v.ncoef);                        // r' = r - A e
+        c.nl += l1 + 2;
+        rem = c.f(v.rp);
+    } else {
         if (cudaMemsetAsync(c.f(v.e), 0, v.ncube * 4, c.st) != cudaSuccess) return DRT3D_ERR_CUDA;
-        if (cudaMemsetAsync(c.f(v.ae), 0, v.ncoef * 4, c.st) != cudaSuccess) return DRT3D_ERR_CUDA;
-        update_x<<<nb, kRedThreads, 0, c.st>>>(c.f(v.e), c.f(v.p), v.ncube, c.alpha(l));
-        update_x<<<nb, kRedThreads, 0, c.st>>>(c.f(v.ae), c.f(v.q), v.ncoef, c.alpha(l));
-        c.nl += 2;
-        return DRT3D_OK;
     }
-    const Level &u = c.L->lv[l + 1];
-    const int K = (int)(v.ncoef / ((size_t)v.n * v.n * 3 * v.n));
-    restrict_coef<<<(unsigned)(K * u.n * u.n), row_threads(3 * u.n), 0, c.st>>>(c.f(v.r), c.f(u.r), u.n);  // S r
+    drt3d_status s = step(c, l, rem);                                                      // alpha, p, q = A p
+    if (s != DRT3D_OK) return s;
+    update_x<<<nb, kRedThreads, 0, c.st>>>(c.f(v.e), c.f(v.p), v.ncube, c.alpha(l));                         // e += a p
     c.nl += 1;
-    drt3d_status s = mg_apply(c, l + 1);                                                                    // B_{n/2}
-    if (s != DRT3D_OK) return s;
-    prolong_cube<<<(unsigned)(v.n * v.n), row_threads(v.n), 0, c.st>>>(c.f(u.e), c.f(v.e), v.n);          // e = P e_c
-    int l1 = 0;
-    c.o.launches = &l1;
-    s = drt3d_planes(c.f(v.e), v.n, c.mask, c.f(v.ae), &c.o, c.tws(), c.L->tws_bytes, c.stream);         // A e
-    if (s != DRT3D_OK) return s;
-    diff<<<nb, kRedThreads, 0, c.st>>>(c.f(v.r), c.f(v.ae), c.f(v.rp), v.ncoef);                          // r' = r - A e
-    c.nl += l1 + 2;
-    s = step(c, l, c.f(v.rp));
-    if (s != DRT3D_OK) return s;
-    update_x<<<nb, kRedThreads, 0, c.st>>>(c.f(v.e), c.f(v.p), v.ncube, c.alpha(l));                       // e += a p
-    update_x<<<nb, kRedThreads, 0, c.st>>>(c.f(v.ae), c.f(v.q), v.ncoef, c.alpha(l));                      // Ae += a q
-    c.nl += 2;
+    if (l == 0) {
+        update_r<<<nb, kRedThreads, 0, c.st>>>(rem, c.f(v.q), c.f(v.r), v.ncoef, c.alpha(l), c.part());      // r = r' - a q
+        c.nl += 1;
+    }
     return DRT3D_OK;
 }
 
@@ -355,12 +372,11 @@ extern "C" drt3d_status drt3d_planes_invert(const void *coef, int N, int n_min, 
         c.nl += 2;
     }
     for (int k = 0; k < iters; ++k) {
-        s = mg_apply(c, 0);                                                              // e = B r, A e
+        s = mg_apply(c, 0);                                                   // e = B r; r <- r - A e
         if (s != DRT3D_OK) return s;
         update_x<<<kRedBlocks, kRedThreads, 0, c.st>>>(x, c.f(top.e), top.ncube, c.one());           // x += e
-        update_r<<<kRedBlocks, kRedThreads, 0, c.st>>>(r, c.f(top.ae), top.ncoef, c.one(), c.part()); // r -= A e
         finalize_norm<<<1, kRedThreads, 0, c.st>>>(c.part(), kRedBlocks, rnorm ? rnorm + k + 1 : nullptr);
-        c.nl += 3;
+        c.nl += 2;
     }
     if (opts && opts->launches) *opts->launches = c.nl;
     return cudaGetLastError() == cudaSuccess ? DRT3D_OK : DRT3D_ERR_CUDA;
