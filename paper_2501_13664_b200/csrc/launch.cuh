@@ -56,10 +56,11 @@ template <int K, class In, class Acc, class Out, bool FIRST, bool FINAL>
 drt3d_status launch_drt_k(const DrtPass &prm_in, int ninst, cudaStream_t st) {
     DrtPass prm = prm_in;
 #ifndef D3_FINAL16_T
-#define D3_FINAL16_T 64
+#define D3_FINAL16_T 48                 // 3 CTAs/SM (70 KB, 128 threads at 168 registers); 64: 2 CTAs/SM, 3.5% slower
 #endif
-    // u16-input passes may use a narrower tile (more resident CTAs per SM)
-    constexpr int R = DrtTile<K>::R, T = (!FIRST && sizeof(In) == 2 && K == 4) ? D3_FINAL16_T : DrtTile<K>::T;
+    // u16-input final passes use a narrower tile (more resident CTAs per SM); non-final passes keep
+    // T / R a power of two (their epilogue shuffles across the T / R runs of a row)
+    constexpr int R = DrtTile<K>::R, T = (!FIRST && FINAL && sizeof(In) == 2 && K == 4) ? D3_FINAL16_T : DrtTile<K>::T;
     if constexpr (!FIRST && FINAL && K == 4 && std::is_same<In, uint16_t>::value && std::is_same<Out, uint32_t>::value) {
         // experiment (measured slower than the default): D3_PERSIST=1
         static const bool no_persist = getenv("D3_PERSIST") == nullptr || getenv("D3_NO_TMA_STORE") != nullptr;
