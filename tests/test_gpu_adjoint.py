@@ -108,3 +108,26 @@ def test_drt_adjoint_single_plane_closed_form(N):
                 if 0 <= z < N:
                     ref[x, y, z] = 1
         assert np.array_equal(got.astype(np.int64), ref), (s1, s2, D)
+
+
+@pytest.mark.parametrize("N", [512, 1024])
+def test_drt_adjoint_single_plane_max_sizes(N):
+    """Three-pass backprojection plans at the largest sizes: one unit coefficient of dodecant 0
+    back-projects to exactly its digital plane (eq:3DfDRT)."""
+    n = N.bit_length() - 1
+    s1, s2, D = N // 3, 2 * N // 3 + 1, N + 11
+    c = torch.zeros((1, N, N, 3 * N), dtype=torch.int32, device="cuda")
+    c[0, s1, s2, D] = 1
+    got = d3.planes_adjoint(c, 0x001)
+    del c
+    nzg = torch.nonzero(got).cpu().numpy()
+    ref = []
+    l1 = [oracle.line(n, s1, u) for u in range(N)]
+    l2 = [oracle.line(n, s2, u) for u in range(N)]
+    for x in range(N):
+        for y in range(N):
+            z = l1[x] + l2[y] + D - 2 * N
+            if 0 <= z < N:
+                ref.append((x, y, z))
+    assert int(got.sum()) == len(ref)
+    assert sorted(map(tuple, nzg.tolist())) == ref

@@ -242,3 +242,63 @@ def test_djt_n128_sampled():
     for _ in range(300):
         s1, s2, D1, D2 = (int(t) for t in rng.integers(0, [N, N, 2 * N, 2 * N]))
         assert host[s1, s2, D1, D2] == oracle.djt_point(cube, s1, s2, D1, D2)
+
+
+# ------------------------------------------------------------ maximum sizes (three-pass plans)
+
+def test_drt_n512_sampled():
+    """N = 512 (three radix passes): two dodecants, mass and support on every column, sampled
+    outputs against eq:3DfDRT by direct summation (oracle.drt_point)."""
+    N, mask = 512, 0x801
+    f = synth.uniform_cube(N, 512, np.uint8)
+    gpu = d3.planes(_gpu(f[None]), mask)[0]                          # [2][N][N][3N] int32, on the device
+    torch.cuda.synchronize()
+    tot = int(f.astype(np.int64).sum())
+    assert bool((gpu.to(torch.int64).sum(dim=3) == tot).all())
+    s = torch.arange(N, device="cuda")
+    lim = 2 * N - s[:, None] - s[None, :]
+    below = torch.arange(3 * N, device="cuda")[None, None, :] < lim[:, :, None]
+    for j in range(2):
+        assert int(gpu[j].masked_select(below).abs().sum()) == 0
+    rows = tables.DRT_HEMISPHERE
+    rng = np.random.default_rng(5)
+    for j, k in enumerate((0, 11)):
+        g = np.ascontiguousarray(oracle.orient(f, rows[k]), dtype=np.float64)   # orient once (1 GB)
+        for _ in range(25):
+            s1, s2 = int(rng.integers(0, N)), int(rng.integers(0, N))
+            Dd = int(rng.integers(2 * N - s1 - s2, 3 * N))
+            assert int(gpu[j, s1, s2, Dd]) == oracle.drt_point(g, s1, s2, Dd)
+
+
+def test_drt_n1024_sparse_sampled():
+    """N = 1024, the largest size the boundary accepts (12.9 GB output for one dodecant): a sparse
+    cube, mass and support on every column, sampled outputs by direct summation over its
+    non-zero voxels with the oracle's digital line (eq:3DfDRT, eq:digitalLine)."""
+    N, n = 1024, 10
+    rng = np.random.default_rng(1024)
+    nz = 3000
+    xs, ys, zs = (rng.integers(0, N, nz) for _ in range(3))
+    vs = rng.integers(1, 256, nz)
+    f = np.zeros((N, N, N), np.uint8)
+    f[xs, ys, zs] = vs
+    xs, ys, zs = np.nonzero(f)
+    vs = f[xs, ys, zs].astype(np.int64)
+    gpu = d3.planes(_gpu(f[None]), 0x001)[0, 0]                      # [N][N][3N] int32 (dodecant 0: identity)
+    torch.cuda.synchronize()
+    assert bool((gpu.to(torch.int64).sum(dim=2) == int(vs.sum())).all())
+    lut = {}
+
+    def line(s, u):
+        key = (s, u)
+        if key not in lut:
+            lut[key] = oracle.line(n, s, u)
+        return lut[key]
+    for _ in range(12):
+        s1, s2 = int(rng.integers(0, N)), int(rng.integers(0, N))
+        ls1 = np.array([line(s1, int(x)) for x in xs])
+        ls2 = np.array([line(s2, int(y)) for y in ys])
+        # every D with a voxel on it, plus random D: the plane through voxel i has D = z - l1 - l2 + 2N
+        Ds = set((zs - ls1 - ls2 + 2 * N).tolist()[:20]) | {int(d) for d in rng.integers(0, 3 * N, 5)}
+        for Dd in Ds:
+            ref = int(vs[zs == ls1 + ls2 + Dd - 2 * N].sum())
+            assert int(gpu[s1, s2, Dd]) == ref
