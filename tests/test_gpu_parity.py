@@ -302,3 +302,20 @@ def test_drt_n1024_sparse_sampled():
         for Dd in Ds:
             ref = int(vs[zs == ls1 + ls2 + Dd - 2 * N].sum())
             assert int(gpu[s1, s2, Dd]) == ref
+
+
+def test_djt_n256_sampled():
+    """N = 256, the largest DJT whose output fits one B200 (4 N^4 int32 = 68.7 GB per dodecant):
+    mass per (s1, s2) plane and sampled outputs against eq:3DfDJT by direct summation."""
+    N = 256
+    cube = synth.uniform_cube(N, 256, np.uint8)
+    gpu = d3.lines(_gpu(cube[None]), 0x001)[0, 0]                    # [N][N][2N][2N] int32 on the device
+    torch.cuda.synchronize()
+    tot = int(cube.astype(np.int64).sum())
+    for s1 in range(0, N, 1):
+        assert bool((gpu[s1].to(torch.int64).sum(dim=(1, 2)) == tot).all()), s1
+    g = np.ascontiguousarray(cube, dtype=np.float64)
+    rng = np.random.default_rng(7)
+    for _ in range(200):
+        s1, s2, D1, D2 = (int(t) for t in rng.integers(0, [N, N, 2 * N, 2 * N]))
+        assert int(gpu[s1, s2, D1, D2]) == oracle.djt_point(g, s1, s2, D1, D2)
