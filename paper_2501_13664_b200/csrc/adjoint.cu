@@ -390,16 +390,27 @@ __global__ void djt_adj_stage(const T *__restrict__ in, T *__restrict__ out, int
 #pragma unroll
     for (int t = 0; t < NT; ++t)
         if (from_coef) row[t] = (row[t] % N) * N + row[t] / N;   // packed s1 + N s2 -> caller row s1 N + s2
-    for (int d1 = d1_0; d1 < d1_0 + kD1 && d1 < W; ++d1) {
-        T *dst = out + ((size_t)i * W + d1) * W;
-        for (int d2 = threadIdx.x; d2 < W; d2 += blockDim.x) {
+    for (int d2 = threadIdx.x; d2 < W; d2 += blockDim.x) {
+        // per-term pointers to (row_t, d1_0 - e1_t, d2 - e2_t), walked down the d1 rows (kept in
+        // registers; dereferenced only where both indices are >= 0)
+        const T *pt[NT];
+        bool ok2[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            pt[t] = in + (((long long)row[t] * W + (d1_0 - e1[t])) * W + (d2 - e2[t]));
+            asm volatile("" : "+l"(pt[t]));
+            ok2[t] = d2 >= e2[t];
+        }
+        T *dst = out + ((size_t)i * W + d1_0) * W + d2;
+        for (int d1 = d1_0; d1 < d1_0 + kD1 && d1 < W; ++d1) {
             T acc = zero_v<T>();
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
-                const int f1 = d1 - e1[t], f2 = d2 - e2[t];
-                if (f1 >= 0 && f2 >= 0) acc = acc + in[((size_t)row[t] * W + f1) * W + f2];
+                if (ok2[t] && d1 >= e1[t]) acc = acc + __ldg(pt[t]);
+                pt[t] += W;
             }
-            dst[d2] = acc;
+            *dst = acc;
+            dst += W;
         }
     }
 }

@@ -48,8 +48,11 @@ struct DjtGeom {
     static_assert(T2 % R == 0 && R % 4 == 0, "tile shape");
 };
 
+#ifndef D3_DJT_MINB
+#define D3_DJT_MINB 1
+#endif
 template <int K, int R, int T1, int T2, class In, class Acc, class Out, bool FIRST, bool FINAL>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, D3_DJT_MINB)
 djt_pass_kernel(const DjtPass p) {
     using G = DjtGeom<K, R, T1, T2>;
     constexpr int S = G::S, WR = G::WR, WC = G::WC, PJ = G::PJ, NR = G::NR;
