@@ -179,13 +179,16 @@ drt3d_status make_plan(int transform, int N, uint32_t mask, const drt3d_opts &o,
                 // the support, rounded down to a chunk so that every reader window starts on one;
                 // the pitch is a whole number of chunks and rows are computed (zero-padded) up to
                 // it, so any chunk inside a row is valid data.
-                // Every origin is a multiple of 16 elements: a pass stages its input from chunk
-                // (D_tile - base_in) / EPC_in with D_tile = base_out + a multiple of its tile width,
-                // so base_out - base_in must be a multiple of the INPUT's chunk (8 for u16, 4 for
-                // 32-bit); and the first pass's vector cube loads need z' = D - 2N on 16 bytes.
-                // (Rounding a 32-bit level to 4 only broke u8 three-pass plans, N >= 512.)
+                // Origin granularity: a pass stages its input from chunk (D_tile - base_in) / EPC_in
+                // with D_tile = base_out + a multiple of its tile width, so base_out - base_in must
+                // be a multiple of the INPUT's chunk (8 for u16, 4 for 32-bit), and the final
+                // origin is 0.  All origins are multiples of 16 when a u16 level is involved (this
+                // level or the one before it: u8 three-pass plans, N >= 512, where a 32-bit level
+                // after a u16 one must not round to 4) -- the first pass's vector cube loads also
+                // want z' = D - 2N on 16 bytes; all-32-bit plans keep 4 (narrower rows at small N).
                 const int epc = 16 / stor_bytes(P.stor[p]);
-                const int gb = 16;
+                const bool u16_near = P.stor[p] == ST_U16 || (p >= 2 && P.stor[p - 1] == ST_U16);
+                const int gb = u16_near ? 16 : epc;
                 P.base[p] = (2 * N - 2 * ((1 << c) - 1) - (epc - 1)) / gb * gb;
                 P.pitch[p] = round_up(3 * N - P.base[p], epc);
                 P.width[p] = P.pitch[p];

@@ -163,7 +163,10 @@ drt3d_status launch_drt(int K, const DrtPass &prm, int ninst, cudaStream_t st) {
 template <int K> struct DjtTile;
 template <> struct DjtTile<1> { static constexpr int R = 8, T1 = 8, T2 = 64; };
 template <> struct DjtTile<2> { static constexpr int R = 8, T1 = 8, T2 = 64; };
-template <> struct DjtTile<3> { static constexpr int R = 8, T1 = 8, T2 = 64; };
+#ifndef D3_DJT3_T1
+#define D3_DJT3_T1 8
+#endif
+template <> struct DjtTile<3> { static constexpr int R = 8, T1 = D3_DJT3_T1, T2 = 64; };
 template <> struct DjtTile<4> { static constexpr int R = 8, T1 = 4, T2 = 64; };
 
 template <int K, class In, class Acc, class Out, bool FIRST, bool FINAL>

@@ -1,7 +1,7 @@
-for v in "" dj4; do
+for v in "" ch1g; do
   if [ -n "$v" ]; then export D3_LIB=$GRAFT_REPO_ROOT/paper_2501_13664_b200/libdrt3d_$v.so; else unset D3_LIB; fi
-  python -m pytest tests/test_gpu_parity.py -q -k "djt" 2>&1 | tail -1
+  echo "== $v"; python tools/fwd_dtypes.py
   python -c "
 import sys; sys.path.insert(0,'tools'); import json, bench_configs as b
-r=b.run(4); print('$v', r['ms_median'])"
+print(json.dumps(b.run_invert(256))[:160]); print(b.run(5)['ms_median'])"
 done
