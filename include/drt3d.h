@@ -185,6 +185,9 @@ drt3d_status drt3d_planes_invert(const void *coef, int N, int n_min, uint32_t do
  *   26-neighbourhood (R21) and whose plane is orthogonal to the argmax plane,
  *   |cos| <= onum/oden, with integer normals through the orientation table
  *   opts->table (R22); *argmax (device int64, may be NULL) receives R20's index.
+ * drt3d_coef_select: out[i] = flags[i] ? coef[i] : 0 (no workspace): with
+ *   drt3d_planes_adjoint it back-projects the detected planes ("When those
+ *   planes are backprojected, they correspond to the walls").
  * Errors: DRT3D_ERR_INVALID_ARG (NULL pointers, n = 0, N, mask, num < 0,
  *   den <= 0, onum < 0, oden <= 0), DRT3D_ERR_WORKSPACE, DRT3D_ERR_CUDA.      */
 size_t drt3d_apps_workspace_size(void);
@@ -192,6 +195,8 @@ drt3d_status drt3d_coef_argmax(const int32_t *coef, size_t n, long long *index, 
                                size_t workspace_bytes, void *stream);
 drt3d_status drt3d_coef_threshold(const int32_t *coef, size_t n, int num, int den, int32_t *out,
                                   void *workspace, size_t workspace_bytes, void *stream);
+drt3d_status drt3d_coef_select(const int32_t *coef, const uint8_t *flags, size_t n, int32_t *out,
+                               void *stream);
 drt3d_status drt3d_detect_planes(const int32_t *coef, int N, uint32_t dodecant_mask, int num, int den,
                                  int onum, int oden, const drt3d_opts *opts, uint8_t *flags,
                                  long long *argmax, void *workspace, size_t workspace_bytes, void *stream);

@@ -29,7 +29,8 @@ C_FUNCTIONS = ("drt3d_status_string", "drt3d_orientation_table", "drt3d_planes_o
                "drt3d_planes_adjoint_workspace_size", "drt3d_planes_adjoint",
                "djt3d_lines_adjoint_workspace_size", "djt3d_lines_adjoint",
                "drt3d_planes_invert_workspace_size", "drt3d_planes_invert",
-               "drt3d_apps_workspace_size", "drt3d_coef_argmax", "drt3d_coef_threshold", "drt3d_detect_planes")
+               "drt3d_apps_workspace_size", "drt3d_coef_argmax", "drt3d_coef_threshold", "drt3d_detect_planes",
+               "drt3d_coef_select")
 
 
 class Drt3dError(RuntimeError):
@@ -90,6 +91,8 @@ def lib() -> ctypes.CDLL:
     L.drt3d_coef_argmax.argtypes = [vp, sz, vp, vp, sz, vp]
     L.drt3d_coef_threshold.restype = i32
     L.drt3d_coef_threshold.argtypes = [vp, sz, i32, i32, vp, vp, sz, vp]
+    L.drt3d_coef_select.restype = i32
+    L.drt3d_coef_select.argtypes = [vp, vp, sz, vp, vp]
     L.drt3d_detect_planes.restype = i32
     L.drt3d_detect_planes.argtypes = [vp, i32, u32, i32, i32, i32, i32, po, vp, vp, vp, sz, vp]
     _lib = L
@@ -353,3 +356,15 @@ def detect_planes(coef, mask: int, num: int, den: int, onum: int, oden: int, tab
     _check(lib().drt3d_detect_planes(c.data_ptr(), N, mask, num, den, onum, oden, ctypes.byref(o), flags.data_ptr(),
                                      am.data_ptr(), ws.data_ptr(), ws.numel(), st), "detect_planes")
     return flags, am
+
+
+def coef_select(coef, flags, out=None, stream=None):
+    """Keep the flagged int32 coefficients (flags uint8 of the same shape), zero the rest."""
+    import torch
+    c, f = coef.contiguous(), flags.contiguous()
+    if not c.is_cuda or c.dtype != torch.int32 or f.dtype != torch.uint8 or f.shape != c.shape:
+        raise Drt3dError("coef: CUDA int32; flags: uint8 of the same shape")
+    out = torch.empty_like(c) if out is None else out
+    st = stream if stream is not None else torch.cuda.current_stream(c.device).cuda_stream
+    _check(lib().drt3d_coef_select(c.data_ptr(), f.data_ptr(), c.numel(), out.data_ptr(), st), "coef_select")
+    return out

@@ -3,6 +3,8 @@
 //   * coefficient threshold (ray denoising, PAPER.md:448 and fig:output3DDJT: "a thresholding of
 //     the highest amplitude coefficients, and subsequent backprojection"): keep c when
 //     c * den >= num * max(c) (reading R19, exact in int64), else 0;
+//   * coefficient selection: keep the flagged coefficients ("When those planes are backprojected,
+//     they correspond to the walls": select, then drt3d_planes_adjoint);
 //   * plane detection: the global argmax plane (R20: ties to the smallest
 //     stacked index), then every coefficient above the R19 threshold that is a relative maximum
 //     in its dodecant's (s1, s2, D) 26-neighbourhood (R21: >= all neighbours, > those with a
@@ -124,6 +126,22 @@ __global__ void threshold_kernel(const int32_t *c, size_t n, int num, int den, c
         reinterpret_cast<int4 *>(out)[v] = make_int4(keep(q.x), keep(q.y), keep(q.z), keep(q.w));
     }
     for (size_t i = 4 * nv + (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) out[i] = keep(c[i]);
+}
+
+// out[i] = flags[i] ? c[i] : 0 (16-byte groups of four; the flags as one 32-bit word)
+__global__ void select_kernel(const int32_t *__restrict__ c, const uint8_t *__restrict__ flags, size_t n,
+                              int32_t *__restrict__ out) {
+    const bool vec = ((reinterpret_cast<uintptr_t>(c) | reinterpret_cast<uintptr_t>(out)) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(flags) & 3) == 0;
+    const size_t nv = vec ? n / 4 : 0, stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += stride) {
+        const int4 q = reinterpret_cast<const int4 *>(c)[v];
+        const uint32_t f = reinterpret_cast<const uint32_t *>(flags)[v];
+        reinterpret_cast<int4 *>(out)[v] = make_int4((f & 0xFFu) ? q.x : 0, (f & 0xFF00u) ? q.y : 0,
+                                                     (f & 0xFF0000u) ? q.z : 0, (f & 0xFF000000u) ? q.w : 0);
+    }
+    for (size_t i = 4 * nv + (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        out[i] = flags[i] ? c[i] : 0;
 }
 
 struct DetectArgs {
@@ -249,6 +267,13 @@ extern "C" drt3d_status drt3d_coef_threshold(const int32_t *coef, size_t n, int 
     const Ws w = carve(ws);
     run_argmax(coef, n, w, nullptr, st);
     threshold_kernel<<<kBlocks, kThreads, 0, st>>>(coef, n, num, den, w.mx, out);
+    return cudaGetLastError() == cudaSuccess ? DRT3D_OK : DRT3D_ERR_CUDA;
+}
+
+extern "C" drt3d_status drt3d_coef_select(const int32_t *coef, const uint8_t *flags, size_t n, int32_t *out,
+                                          void *stream) {
+    if (!coef || !flags || !out || n == 0) return DRT3D_ERR_INVALID_ARG;
+    select_kernel<<<kBlocks, kThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(coef, flags, n, out);
     return cudaGetLastError() == cudaSuccess ? DRT3D_OK : DRT3D_ERR_CUDA;
 }
 

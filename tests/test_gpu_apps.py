@@ -110,3 +110,26 @@ def test_denoise_recovers_ray_large():
     assert d3.coef_argmax(c) == np.ravel_multi_index((0, s1, s2, d1, d2), c.shape)
     top = np.argsort(back.reshape(-1))[::-1][:N]
     assert set(top.tolist()) == set(np.flatnonzero(ray).tolist())
+
+
+def test_select_and_backproject_walls():
+    """"When those planes are backprojected, they correspond to the walls": select the
+    detected coefficients and back-project them (bit-exact against the oracle's adjoint of the
+    same selection); every wall voxel lies on its detected wall plane, whose coefficient is >= N^2."""
+    N = 32
+    f = _room(N, 1)
+    c = d3.planes(torch.from_numpy(f).cuda(), 0xFFF)
+    flags, _ = d3.detect_planes(c, 0xFFF, 1, 3, 1, 10)
+    sel = d3.coef_select(c, flags)
+    back = d3.planes_adjoint(sel, 0xFFF)
+    torch.cuda.synchronize()
+    cn, fn = c.cpu().numpy().astype(np.int64), flags.cpu().numpy()
+    assert np.array_equal(sel.cpu().numpy().astype(np.int64), np.where(fn != 0, cn, 0))
+    ref = oracle.drt_planes_adjoint(np.where(fn != 0, cn, 0), 0xFFF)
+    b = back.cpu().numpy().astype(np.int64)
+    assert np.array_equal(b, ref)
+    wall = np.zeros((N, N, N), bool)
+    wall[3] = True
+    wall[:, N - 4] = True
+    wall[:, :, 2] = True
+    assert b[wall].min() >= N * N
