@@ -43,7 +43,10 @@ struct DjtGeom {
     static constexpr int PJ0 = ((NEED > WC ? NEED : WC) + 3) / 4 * 4;
     static constexpr int PJ = ((PJ0 / 4) % 2 == 1) ? PJ0 : PJ0 + 4;   // pitch/4 odd: no bank conflicts across rows
     static constexpr int TASKS = S * T1 * NR;
-    static constexpr int THREADS = 256;
+#ifndef D3_DJT_THREADS
+#define D3_DJT_THREADS 128    // 4 CTAs per SM at ~100 registers; 256 (2 per SM) is 1.7% slower on cfg4
+#endif
+    static constexpr int THREADS = D3_DJT_THREADS;
     static constexpr int SMEM = S * WR * PJ * 4;
     static_assert(T2 % R == 0 && R % 4 == 0, "tile shape");
 };
@@ -52,7 +55,7 @@ struct DjtGeom {
 #define D3_DJT_MINB 1
 #endif
 template <int K, int R, int T1, int T2, class In, class Acc, class Out, bool FIRST, bool FINAL>
-__global__ void __launch_bounds__(256, D3_DJT_MINB)
+__global__ void __launch_bounds__(D3_DJT_THREADS, D3_DJT_MINB)
 djt_pass_kernel(const DjtPass p) {
     using G = DjtGeom<K, R, T1, T2>;
     constexpr int S = G::S, WR = G::WR, WC = G::WC, PJ = G::PJ, NR = G::NR;
