@@ -455,11 +455,8 @@ int adj_fuse() {
 template <class T, int L, int NC>
 void drt_bfly_nc(const T *in, T *out, int N, int m_lo, cudaStream_t st) {
     const size_t smem = (size_t)(1 << (2 * L)) * 3 * N * sizeof(T);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(drt_adj_bfly<T, L, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-    }
+    static std::atomic<uint32_t> smem_done{0};
+    set_smem_once(drt_adj_bfly<T, L, NC>, 200 * 1024, smem_done);
     drt_adj_bfly<T, L, NC><<<(unsigned)((N >> L) * (N >> L)), 256, smem, st>>>(in, out, N, m_lo);
 }
 
@@ -529,13 +526,8 @@ constexpr int kAdjT = 64, kAdjR = 8;
 template <int K, class T>
 void launch_adj_pass(const AdjPass &a, int ntiles, int groups, int D, cudaStream_t st) {
     using G = DrtGeom<K, kAdjR, kAdjT, false>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(drt_adj_pass_kernel<K, kAdjR, kAdjT, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        cudaFuncSetAttribute(drt_adj_pass_kernel<K, kAdjR, kAdjT, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             G::SMEM);
-        attr = true;
-    }
+    static std::atomic<uint32_t> smem_done{0};
+    set_smem_once(drt_adj_pass_kernel<K, kAdjR, kAdjT, T>, G::SMEM, smem_done);
     drt_adj_pass_kernel<K, kAdjR, kAdjT, T><<<dim3((unsigned)ntiles, (unsigned)groups, (unsigned)D), G::THREADS, G::SMEM,
                                                st>>>(a);
 }

@@ -1,11 +1,37 @@
 // common.cuh -- device/host helpers shared by the DRT and DJT kernels of the
 // B200 library (product code; independent of oracle/).
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <type_traits>
 #include <cuda_runtime.h>
 
 namespace d3 {
+
+// ---- host: kernel attributes
+template <class KernelT>
+bool set_smem(KernelT k, int bytes) {
+    // prefer the maximum shared-memory carveout so two CTAs of ~100 KB fit on one SM
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (bytes <= 48 * 1024) return true;
+    return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess;
+}
+
+// set_smem once per kernel and device: `done` is one bit per device, a static of the caller's
+// launcher instantiation (one per kernel; a static here would be shared by every kernel of the
+// same signature).  Function attributes are per device, so a process driving several GPUs sets
+// them on each; racing threads may both set them, which is harmless.
+template <class KernelT>
+bool set_smem_once(KernelT k, int bytes, std::atomic<uint32_t> &done) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint32_t bit = 1u << (dev & 31);
+    if (done.load(std::memory_order_acquire) & bit) return true;
+    const bool ok = set_smem(k, bytes);
+    if (ok) done.fetch_or(bit, std::memory_order_release);
+    return ok;
+}
+
 
 // eq:digitalLine, recursive form, restated for the GPU path:
 //   l^k_s(u) = l^{k-1}_{floor(s/2)}(u mod 2^{k-1}) + u_{k-1} * floor((s+1)/2).

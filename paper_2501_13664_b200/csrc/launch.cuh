@@ -11,14 +11,6 @@
 
 namespace d3 {
 
-template <class KernelT>
-bool set_smem(KernelT k, int bytes) {
-    // prefer the maximum shared-memory carveout so two CTAs of ~100 KB fit on one SM
-    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (bytes <= 48 * 1024) return true;
-    return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess;
-}
-
 // ---- DRT kernel selection
 template <int K> struct DrtTile;
 template <> struct DrtTile<1> { static constexpr int R = 8, T = 128; };
@@ -71,8 +63,8 @@ drt3d_status launch_drt_k(const DrtPass &prm_in, int ninst, cudaStream_t st) {
             // persistent two-CTA/SM final pass with overlapped staging and deferred TMA stores
             using QG = PersistGeom<K, R, TQ>;
             auto kern = drt_final_persist_kernel<K, R, TQ>;
-            static bool attr_ok = set_smem(kern, QG::SMEM);
-            if (!attr_ok) return DRT3D_ERR_CUDA;
+            static std::atomic<uint32_t> smem_done{0};
+            if (!set_smem_once(kern, QG::SMEM, smem_done)) return DRT3D_ERR_CUDA;
             CUtensorMap omap;
             if (!make_out_map(&omap, prm.out, prm.N, prm.inst_total, TQ, 1 << K)) return DRT3D_ERR_CUDA;
             static int nsm = [] {
@@ -94,8 +86,8 @@ drt3d_status launch_drt_k(const DrtPass &prm_in, int ninst, cudaStream_t st) {
             constexpr int TP = 48;                      // 4 X + 3 Y + 1 producer warps: 255 regs/thread
             using PG = PipeGeom<K, R, TP>;
             auto kern = drt_final_pipe_kernel<K, R, TP>;
-            static bool attr_ok = set_smem(kern, PG::SMEM);
-            if (!attr_ok) return DRT3D_ERR_CUDA;
+            static std::atomic<uint32_t> smem_done{0};
+            if (!set_smem_once(kern, PG::SMEM, smem_done)) return DRT3D_ERR_CUDA;
             static int nsm = [] {
                 int dev = 0, v = 0;
                 cudaGetDevice(&dev);
@@ -119,8 +111,8 @@ drt3d_status launch_drt_k(const DrtPass &prm_in, int ninst, cudaStream_t st) {
         constexpr int RS = SWAR_R;
         using SG = SwarGeom<K, RS, T>;
         auto kern = drt_first_swar_kernel<K, RS, T>;
-        static bool attr_ok = set_smem(kern, SG::SMEM);
-        if (!attr_ok) return DRT3D_ERR_CUDA;
+        static std::atomic<uint32_t> smem_done{0};
+        if (!set_smem_once(kern, SG::SMEM, smem_done)) return DRT3D_ERR_CUDA;
         const int ntiles = (prm.out_width + 8 + T - 1) / T;
         dim3 grid(ntiles, (unsigned)(1LL << (2 * prm.m)), ninst);
         kern<<<grid, SG::THREADS, SG::SMEM, st>>>(prm);
@@ -128,8 +120,8 @@ drt3d_status launch_drt_k(const DrtPass &prm_in, int ninst, cudaStream_t st) {
     }
     using G = DrtGeom<K, R, T, !FIRST && sizeof(In) == 2>;
     auto kern = drt_pass_kernel<K, R, T, In, Acc, Out, FIRST, FINAL>;
-    static bool attr_ok = set_smem(kern, G::SMEM);
-    if (!attr_ok) return DRT3D_ERR_CUDA;
+    static std::atomic<uint32_t> smem_done{0};
+    if (!set_smem_once(kern, G::SMEM, smem_done)) return DRT3D_ERR_CUDA;
     // intermediate outputs are stored pre-shifted by up to one chunk: cover one extra chunk
     const int ntiles = (prm.out_width + (FINAL ? 0 : 16 / (int)sizeof(Out)) + T - 1) / T;
     const long long groups = 1LL << (2 * (prm.c + prm.m));
@@ -174,8 +166,8 @@ drt3d_status launch_djt_k(DjtPass prm, int ninst, cudaStream_t st) {
     constexpr int R = DjtTile<K>::R, T1 = DjtTile<K>::T1, T2 = DjtTile<K>::T2;
     using G = DjtGeom<K, R, T1, T2>;
     auto kern = djt_pass_kernel<K, R, T1, T2, In, Acc, Out, FIRST, FINAL>;
-    static bool attr_ok = set_smem(kern, G::SMEM);
-    if (!attr_ok) return DRT3D_ERR_CUDA;
+    static std::atomic<uint32_t> smem_done{0};
+    if (!set_smem_once(kern, G::SMEM, smem_done)) return DRT3D_ERR_CUDA;
     const int nt1 = (prm.out_width + T1 - 1) / T1, nt2 = (prm.out_width + T2 - 1) / T2;
     prm.nt2 = nt2;
     const long long groups = (1LL << (2 * prm.c)) << prm.m;
