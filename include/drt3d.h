@@ -125,6 +125,8 @@ drt3d_status djt3d_lines(const void *cube, int N, uint32_t dodecant_mask, void *
  * planes, [batch][K][N][N][2N][2N] for lines) with element type opts->out_dtype
  * (I32: exact sums mod 2^32; F32: fp32 accumulation); cube: [batch][N][N][N]
  * of the same element type (opts->in_dtype is ignored).  STACKED layout only.
+ * coef and cube must be 16-byte aligned, the workspace 256-byte aligned
+ * (DRT3D_ERR_INVALID_ARG / DRT3D_ERR_WORKSPACE otherwise).
  * Workspace: query the size (it depends on N and on the number of dodecants:
  * the DRT runs the dodecants of a chunk together, up to 4 GB of level
  * buffers -- all 12 at N = 256, 1.7 GB).                                     */
@@ -159,8 +161,8 @@ drt3d_status djt3d_lines_adjoint(const void *coef, int N, uint32_t dodecant_mask
  * workspaces (query the size; 256-byte aligned).
  * Enqueue only: every iteration runs on `stream` with no host synchronisation
  * (the step sizes live in the workspace).
- * Errors: DRT3D_ERR_INVALID_ARG (N, n_min, mask, opts, NULL pointers,
- * iters < 0), DRT3D_ERR_WORKSPACE, DRT3D_ERR_CUDA.                           */
+ * Errors: DRT3D_ERR_INVALID_ARG (N, n_min, mask, opts, NULL or not 16-byte
+ * aligned coef / cube, iters < 0), DRT3D_ERR_WORKSPACE, DRT3D_ERR_CUDA.      */
 drt3d_status drt3d_planes_invert_workspace_size(int N, int n_min, uint32_t dodecant_mask,
                                                 const drt3d_opts *opts, size_t *bytes);
 drt3d_status drt3d_planes_invert(const void *coef, int N, int n_min, uint32_t dodecant_mask, int iters,

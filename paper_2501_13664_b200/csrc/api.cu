@@ -598,7 +598,10 @@ static drt3d_status adjoint_run(int transform, const void *coef, int N, uint32_t
     drt3d_status s = adjoint_check(transform, N, mask, o, n);
     if (s != DRT3D_OK) return s;
     if (!coef || !cube) return DRT3D_ERR_INVALID_ARG;
+    // 16-byte staging copies / vector stores, like the forward transform
+    if ((reinterpret_cast<uintptr_t>(coef) | reinterpret_cast<uintptr_t>(cube)) & 15) return DRT3D_ERR_INVALID_ARG;
     if (!ws || ws_bytes < d3::adjoint_workspace_bytes(transform, N, mask)) return DRT3D_ERR_WORKSPACE;
+    if (reinterpret_cast<uintptr_t>(ws) & 255) return DRT3D_ERR_WORKSPACE;
     const int K = popcount12(mask);
     const size_t cb = (size_t)o.batch * N * N * N * 4;
     const size_t ob = (size_t)o.batch * K * N * N * (transform == 0 ? 3 * N : 4 * N * N) * 4;

@@ -352,6 +352,7 @@ extern "C" drt3d_status drt3d_planes_invert(const void *coef, int N, int n_min, 
     drt3d_status s = invert_check(N, n_min, mask, opts, table);
     if (s != DRT3D_OK) return s;
     if (!coef || !cube || iters < 0) return DRT3D_ERR_INVALID_ARG;
+    if ((reinterpret_cast<uintptr_t>(coef) | reinterpret_cast<uintptr_t>(cube)) & 15) return DRT3D_ERR_INVALID_ARG;
     Layout L;
     s = layout(N, n_min, mask, table, L);
     if (s != DRT3D_OK) return s;

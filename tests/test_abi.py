@@ -90,3 +90,62 @@ def test_null_and_workspace_errors():
     assert d3.djt3d_lines(16, 64, 1, 1 << 40, o, None, 0, None) == d3.DRT3D_ERR_WORKSPACE
     assert d3.djt3d_lines(16, 64, 1, (1 << 40) + 4, o, None, 0, None) == d3.DRT3D_ERR_INVALID_ARG  # misaligned out
     assert d3.status_string(d3.DRT3D_ERR_CUDA) == "DRT3D_ERR_CUDA"
+
+
+def _size(fn, *args):
+    b = ctypes.c_size_t(0)
+    s = fn(*args, ctypes.byref(b))
+    return s, b.value
+
+
+def test_adjoint_invert_apps_sizes():
+    L = d3.lib()
+    o32 = d3.make_opts(in_dtype=d3.DRT3D_I32, out_dtype=d3.DRT3D_I32)
+    s, a256 = _size(L.drt3d_planes_adjoint_workspace_size, 256, 0xFFF, ctypes.byref(o32))
+    assert s == d3.DRT3D_OK and 1 << 30 < a256 < 4 << 30               # 12 dodecants per chunk at N = 256
+    s, a1 = _size(L.drt3d_planes_adjoint_workspace_size, 256, 0x001, ctypes.byref(o32))
+    assert s == d3.DRT3D_OK and a1 < a256
+    s, j64 = _size(L.djt3d_lines_adjoint_workspace_size, 64, 0x001, ctypes.byref(o32))
+    assert s == d3.DRT3D_OK and j64 >= 2 * 64 * 64 * 128 * 128 * 4
+    of = d3.make_opts(in_dtype=d3.DRT3D_F32, out_dtype=d3.DRT3D_F32)
+    s, i2 = _size(L.drt3d_planes_invert_workspace_size, 64, 2, 0xFFF, ctypes.byref(of))
+    s2, i64 = _size(L.drt3d_planes_invert_workspace_size, 64, 64, 0xFFF, ctypes.byref(of))
+    assert s == s2 == d3.DRT3D_OK and i64 < i2                         # single grid needs fewer levels
+    assert L.drt3d_apps_workspace_size() >= 256
+
+
+def test_adjoint_invert_apps_validation():
+    """Every rejection happens on the host before any launch (bogus device pointers)."""
+    L = d3.lib()
+    bogus, mis = 1 << 40, (1 << 40) + 4
+    o32 = d3.make_opts(in_dtype=d3.DRT3D_I32, out_dtype=d3.DRT3D_I32)
+    po = ctypes.byref(o32)
+    E, W = d3.DRT3D_ERR_INVALID_ARG, d3.DRT3D_ERR_WORKSPACE
+    assert L.drt3d_planes_adjoint(bogus, 12, 0xFFF, bogus, po, bogus, 1 << 40, None) == E     # N not 2^k
+    assert L.drt3d_planes_adjoint(bogus, 16, 0x0, bogus, po, bogus, 1 << 40, None) == E       # empty mask
+    assert L.drt3d_planes_adjoint(None, 16, 0x1, bogus, po, bogus, 1 << 40, None) == E
+    assert L.drt3d_planes_adjoint(mis, 16, 0x1, bogus, po, bogus, 1 << 40, None) == E         # misaligned coef
+    assert L.drt3d_planes_adjoint(bogus, 16, 0x1, mis, po, bogus, 1 << 40, None) == E         # misaligned cube
+    assert L.drt3d_planes_adjoint(bogus, 16, 0x1, bogus << 2, po, None, 0, None) == W
+    assert L.drt3d_planes_adjoint(bogus, 16, 0x1, bogus << 2, po, bogus + 16, 1 << 40, None) == W   # ws alignment
+    assert L.djt3d_lines_adjoint(bogus, 16, 0x1, bogus << 2, po, None, 0, None) == W
+    u8 = d3.make_opts(in_dtype=d3.DRT3D_U8, out_dtype=d3.DRT3D_U8)
+    assert L.drt3d_planes_adjoint(bogus, 16, 0x1, bogus << 2, ctypes.byref(u8), bogus, 1 << 40, None) == E
+    of = d3.make_opts(in_dtype=d3.DRT3D_F32, out_dtype=d3.DRT3D_F32)
+    pf = ctypes.byref(of)
+    assert L.drt3d_planes_invert(bogus, 16, 3, 0xFFF, 2, bogus, None, pf, bogus, 1 << 40, None) == E   # n_min not 2^k
+    assert L.drt3d_planes_invert(bogus, 16, 32, 0xFFF, 2, bogus, None, pf, bogus, 1 << 40, None) == E  # n_min > N
+    assert L.drt3d_planes_invert(bogus, 16, 2, 0xFFF, -1, bogus, None, pf, bogus, 1 << 40, None) == E  # iters < 0
+    assert L.drt3d_planes_invert(mis, 16, 2, 0xFFF, 2, bogus, None, pf, bogus, 1 << 40, None) == E
+    assert L.drt3d_planes_invert(bogus, 16, 2, 0xFFF, 2, bogus, None, ctypes.byref(o32), bogus, 1 << 40, None) == E
+    assert L.drt3d_planes_invert(bogus, 16, 2, 0xFFF, 2, bogus, None, pf, None, 0, None) == W
+    ob = d3.make_opts(in_dtype=d3.DRT3D_F32, out_dtype=d3.DRT3D_F32, batch=2)
+    assert L.drt3d_planes_invert(bogus, 16, 2, 0xFFF, 2, bogus, None, ctypes.byref(ob), bogus, 1 << 40, None) == E
+    ws = L.drt3d_apps_workspace_size()
+    assert L.drt3d_coef_argmax(bogus, 0, bogus, bogus, ws, None) == E                         # empty array
+    assert L.drt3d_coef_argmax(bogus, 10, bogus, bogus, ws - 1, None) == W
+    assert L.drt3d_coef_threshold(bogus, 10, 1, 0, bogus, bogus, ws, None) == E                # den = 0
+    assert L.drt3d_coef_threshold(bogus, 10, -1, 2, bogus, bogus, ws, None) == E               # num < 0
+    assert L.drt3d_detect_planes(bogus, 12, 0xFFF, 1, 3, 1, 10, None, bogus, None, bogus, ws, None) == E
+    assert L.drt3d_detect_planes(bogus, 16, 0xFFF, 1, 3, 1, 0, None, bogus, None, bogus, ws, None) == E
+    assert L.drt3d_coef_select(bogus, None, 10, bogus, None) == E
