@@ -90,7 +90,11 @@ struct DrtGeom {
     // CTAS resident CTAs per SM (shared memory bound); with W warps per CTA one SM sub-partition
     // holds ceil(CTAS W / 4) warps of its 16K-register file, which caps the registers per thread
     static constexpr int CTAS0 = (227 * 1024) / (SMEM + 1024);
-    static constexpr int CTAS = CTAS0 < 1 ? 1 : (CTAS0 > 4 ? 4 : CTAS0);
+#ifndef D3_CTAS_MAX
+#define D3_CTAS_MAX 8      // small-SMEM 32-bit passes (N <= 64): more resident CTAs, fewer registers;
+                           // swept 4 / 6 / 8 / 10 / 12: 8 best (cfg5 0.860 -> 0.825 ms, cfg2 -4%)
+#endif
+    static constexpr int CTAS = CTAS0 < 1 ? 1 : (CTAS0 > D3_CTAS_MAX ? D3_CTAS_MAX : CTAS0);
     static constexpr int MAXREG0 = 16384 / (((CTAS * WARPS + 3) / 4) * 32) / 8 * 8;
     static constexpr int MAXREG = MAXREG0 > 255 ? 255 : MAXREG0;
     static_assert(T % R == 0 && R % 8 == 0, "tile shape");
