@@ -9,6 +9,8 @@
 // recurse to N/2, prolongate, then one filtered-backprojection step on what remains; the
 // coarsest size n_min takes the step alone (n_min = N: single-grid iteration).
 //
+// Iteration 1 is enqueued directly; the others replay one captured iteration (a CUDA graph, cached
+// per buffers and shapes; ~100 launches per iteration at N = 64 become one).
 // Every iteration is enqueued on the caller's stream with no host synchronisation: A^T is the
 // library's backprojection, A its forward transform (fp32 in / fp32 out), and alpha is computed
 // on the device by a fixed-order two-pass fp64 reduction (deterministic) and read by the update
@@ -16,6 +18,7 @@
 #include "drt3d.h"
 
 #include <cstdint>
+#include <mutex>
 
 #include <cuda_runtime.h>
 
@@ -104,6 +107,21 @@ __global__ void __launch_bounds__(kRedThreads) sum_sq(const float *__restrict__ 
     const double s = block_sum(rr, sh);
     if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
+
+// out[*ctr] = sqrt(sum part), then ++*ctr: the residual-norm slot of an iteration comes from
+// device memory, so one captured iteration (a CUDA graph) serves every iteration
+__global__ void finalize_norm_ctr(const double *__restrict__ part, int nb, double *__restrict__ out, int *ctr) {
+    __shared__ double sh[kRedThreads / 32];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) s += part[i];
+    const double t = block_sum(s, sh);
+    if (threadIdx.x == 0) {
+        if (out) out[*ctr] = sqrt(t);
+        *ctr += 1;
+    }
+}
+
+__global__ void set_int(int *p, int v) { *p = v; }
 
 __global__ void finalize_norm(const double *__restrict__ part, int nb, double *__restrict__ out) {
     __shared__ double sh[kRedThreads / 32];
@@ -232,7 +250,8 @@ inline drt3d_status layout(int N, int n_min, uint32_t mask, int table, Layout &L
         v.p = off; off += align256(v.ncube * 4);
     }
     L.part = off; off += align256(2 * kRedBlocks * sizeof(double));
-    L.scal = off; off += 256;                           // [0] = 1.0, [1 + l] = alpha of level l
+    L.scal = off; off += 256;                           // [0] = 1.0, [1 + l] = alpha of level l, int at +128
+    static_assert(8 * (1 + kMaxLevels) <= 128, "scalar slots");
     L.tws = off; off += L.tws_bytes;
     L.total = off;
     return DRT3D_OK;
@@ -279,10 +298,12 @@ struct Ctx {
     void *stream;
     drt3d_opts o;
     int nl;
+    double *rnorm;
     float *f(size_t off) const { return reinterpret_cast<float *>(w + off); }
     double *part() const { return reinterpret_cast<double *>(w + L->part); }
     double *one() const { return reinterpret_cast<double *>(w + L->scal); }
     double *alpha(int l) const { return reinterpret_cast<double *>(w + L->scal) + 1 + l; }
+    int *ctr() const { return reinterpret_cast<int *>(w + L->scal + 128); }
     void *tws() const { return w + L->tws; }
 };
 
@@ -343,6 +364,70 @@ drt3d_status mg_apply(Ctx &c, int l) {
     return DRT3D_OK;
 }
 
+// one outer iteration: e = B r, r <- r - A e (in mg_apply), x += e, ||r|| into rnorm[ctr++]
+drt3d_status iteration(Ctx &c, float *x) {
+    const Level &top = c.L->lv[0];
+    drt3d_status s = mg_apply(c, 0);
+    if (s != DRT3D_OK) return s;
+    update_x<<<kRedBlocks, kRedThreads, 0, c.st>>>(x, c.f(top.e), top.ncube, c.one());
+    finalize_norm_ctr<<<1, kRedThreads, 0, c.st>>>(c.part(), kRedBlocks, c.rnorm, c.ctr());
+    c.nl += 2;
+    return DRT3D_OK;
+}
+
+// Instantiated one-iteration graphs, keyed by everything they bake in.  Kept for the life of the
+// process (a graph may still be executing when the call returns, so none is destroyed); at most
+// kGraphCache entries, beyond which calls fall back to eager enqueue.
+struct GraphKey {
+    int dev, N, n_min, mask, table;
+    const void *x, *rnorm, *ws;
+    bool operator==(const GraphKey &o) const {
+        return dev == o.dev && N == o.N && n_min == o.n_min && mask == o.mask && table == o.table && x == o.x &&
+               rnorm == o.rnorm && ws == o.ws;
+    }
+};
+constexpr int kGraphCache = 16;
+
+cudaGraphExec_t graph_for(GraphKey key, Ctx &c, float *x) {
+    static std::mutex mu;
+    static GraphKey keys[kGraphCache];
+    static cudaGraphExec_t execs[kGraphCache];
+    static int count = 0;
+    static cudaStream_t capture_stream[32] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    key.dev = dev;
+    std::lock_guard<std::mutex> lock(mu);
+    for (int i = 0; i < count; ++i)
+        if (keys[i] == key) return execs[i];
+    if (count == kGraphCache || dev >= 32) return nullptr;
+    // capture on an internal stream (capture is illegal on the legacy default stream, which the
+    // caller may use); nothing executes during capture
+    if (!capture_stream[dev] && cudaStreamCreateWithFlags(&capture_stream[dev], cudaStreamNonBlocking) != cudaSuccess)
+        return nullptr;
+    Ctx cc = c;
+    cc.st = capture_stream[dev];
+    cc.stream = capture_stream[dev];
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    if (cudaStreamBeginCapture(cc.st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    const drt3d_status s = iteration(cc, x);
+    const cudaError_t e = cudaStreamEndCapture(cc.st, &graph);
+    if (s != DRT3D_OK || e != cudaSuccess || !graph || cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+        if (graph) cudaGraphDestroy(graph);
+        cudaGetLastError();
+        return nullptr;
+    }
+    cudaGraphDestroy(graph);                                  // the executable keeps its own copy
+    keys[count] = key;
+    execs[count] = exec;
+    ++count;
+    return exec;
+}
+
 }  // namespace
 
 extern "C" drt3d_status drt3d_planes_invert(const void *coef, int N, int n_min, uint32_t mask, int iters, void *cube,
@@ -358,7 +443,7 @@ extern "C" drt3d_status drt3d_planes_invert(const void *coef, int N, int n_min, 
     if (s != DRT3D_OK) return s;
     if (!ws || ws_bytes < L.total || (reinterpret_cast<uintptr_t>(ws) & 255)) return DRT3D_ERR_WORKSPACE;
     Ctx c{&L, reinterpret_cast<unsigned char *>(ws), mask, reinterpret_cast<cudaStream_t>(stream), stream,
-          f32_opts(table), 0};
+          f32_opts(table), 0, nullptr};
     const Level &top = L.lv[0];
     float *x = reinterpret_cast<float *>(cube), *r = c.f(top.r);
     static const double kOne = 1.0;
@@ -367,17 +452,34 @@ extern "C" drt3d_status drt3d_planes_invert(const void *coef, int N, int n_min, 
     // x0 = 0, r0 = b
     if (cudaMemsetAsync(x, 0, top.ncube * 4, c.st) != cudaSuccess) return DRT3D_ERR_CUDA;
     if (cudaMemcpyAsync(r, coef, top.ncoef * 4, cudaMemcpyDeviceToDevice, c.st) != cudaSuccess) return DRT3D_ERR_CUDA;
+    c.rnorm = rnorm;
     if (rnorm) {
         sum_sq<<<kRedBlocks, kRedThreads, 0, c.st>>>(r, top.ncoef, c.part());
         finalize_norm<<<1, kRedThreads, 0, c.st>>>(c.part(), kRedBlocks, rnorm);
         c.nl += 2;
     }
-    for (int k = 0; k < iters; ++k) {
-        s = mg_apply(c, 0);                                                   // e = B r; r <- r - A e
-        if (s != DRT3D_OK) return s;
-        update_x<<<kRedBlocks, kRedThreads, 0, c.st>>>(x, c.f(top.e), top.ncube, c.one());           // x += e
-        finalize_norm<<<1, kRedThreads, 0, c.st>>>(c.part(), kRedBlocks, rnorm ? rnorm + k + 1 : nullptr);
-        c.nl += 2;
+    set_int<<<1, 1, 0, c.st>>>(c.ctr(), 1);
+    c.nl += 1;
+    if (iters == 0) {
+        if (opts && opts->launches) *opts->launches = c.nl;
+        return cudaGetLastError() == cudaSuccess ? DRT3D_OK : DRT3D_ERR_CUDA;
+    }
+    // iteration 1 eagerly (it also sets every kernel attribute), the others by replaying one
+    // captured iteration
+    s = iteration(c, x);
+    if (s != DRT3D_OK) return s;
+    if (iters > 1) {
+        const GraphKey key{0, N, n_min, (int)mask, table, x, rnorm, ws};
+        cudaGraphExec_t exec = graph_for(key, c, x);
+        for (int k = 1; k < iters; ++k) {
+            if (exec) {
+                if (cudaGraphLaunch(exec, c.st) != cudaSuccess) return DRT3D_ERR_CUDA;
+                c.nl += 1;
+            } else {
+                s = iteration(c, x);
+                if (s != DRT3D_OK) return s;
+            }
+        }
     }
     if (opts && opts->launches) *opts->launches = c.nl;
     return cudaGetLastError() == cudaSuccess ? DRT3D_OK : DRT3D_ERR_CUDA;
