@@ -319,3 +319,30 @@ def test_djt_n256_sampled():
     for _ in range(200):
         s1, s2, D1, D2 = (int(t) for t in rng.integers(0, [N, N, 2 * N, 2 * N]))
         assert int(gpu[s1, s2, D1, D2]) == oracle.djt_point(g, s1, s2, D1, D2)
+
+
+def test_drt_batched_multichunk_overlap():
+    """9 cubes x 12 dodecants at N=128 (108 instances of 5.2 MB stage buffers: more than one
+    512 MB chunk), so the call runs several chunks with the cross-stream overlap and alternating
+    buffer sets: every cube's result equals its single-cube call, and
+    sampled outputs equal the oracle's direct sums."""
+    N, B = 128, 9
+    cubes = synth.uniform_cube(N, 900, np.uint8, batch=B).reshape(B, N, N, N)
+    o = d3.make_opts(batch=B, in_dtype=d3.DRT3D_U8, out_dtype=d3.DRT3D_I32)
+    ws = d3.drt3d_planes_workspace_size(N, 0xFFF, o)
+    o1 = d3.make_opts(batch=1, in_dtype=d3.DRT3D_U8, out_dtype=d3.DRT3D_I32)
+    assert ws > d3.drt3d_planes_workspace_size(N, 0xFFF, o1)          # several chunks, two buffer sets
+    got = d3.planes(_gpu(cubes), 0xFFF)                              # [B][12][N][N][3N]
+    for b in (0, 4, 8):
+        one = d3.planes(_gpu(cubes[b][None]), 0xFFF)[0]
+        assert bool(torch.equal(got[b], one)), b
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(9)
+    rows = tables.DRT_HEMISPHERE
+    for b in (0, 8):
+        for k in (0, 7):
+            g = np.ascontiguousarray(oracle.orient(cubes[b], rows[k]), dtype=np.float64)
+            for _ in range(10):
+                s1, s2 = int(rng.integers(0, N)), int(rng.integers(0, N))
+                Dd = int(rng.integers(2 * N - s1 - s2, 3 * N))
+                assert int(got[b, k, s1, s2, Dd]) == oracle.drt_point(g, s1, s2, Dd)
