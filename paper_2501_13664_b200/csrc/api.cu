@@ -322,8 +322,12 @@ struct L2Window {
 struct Aux {
     cudaStream_t a = nullptr;
     cudaEvent_t start = nullptr, fdone = nullptr, cdone[2] = {nullptr, nullptr};
+    // host-buffer calls: device-to-host copies of finished dodecant groups (kHostGroups max)
+    cudaStream_t cp = nullptr;
+    cudaEvent_t gdone[4] = {nullptr, nullptr, nullptr, nullptr}, cpdone = nullptr;
     bool ok = false;
 };
+constexpr int kHostGroups = 4;
 Aux *aux_for_current_device() {
     thread_local Aux aux[16];
     int dev = 0;
@@ -335,6 +339,10 @@ Aux *aux_for_current_device() {
         e = e && cudaEventCreateWithFlags(&x.fdone, cudaEventDisableTiming) == cudaSuccess;
         e = e && cudaEventCreateWithFlags(&x.cdone[0], cudaEventDisableTiming) == cudaSuccess;
         e = e && cudaEventCreateWithFlags(&x.cdone[1], cudaEventDisableTiming) == cudaSuccess;
+        e = e && cudaStreamCreateWithFlags(&x.cp, cudaStreamNonBlocking) == cudaSuccess;
+        for (int g = 0; g < kHostGroups; ++g)
+            e = e && cudaEventCreateWithFlags(&x.gdone[g], cudaEventDisableTiming) == cudaSuccess;
+        e = e && cudaEventCreateWithFlags(&x.cpdone, cudaEventDisableTiming) == cudaSuccess;
         if (!e) return nullptr;
         x.ok = true;
     }
@@ -641,6 +649,42 @@ static drt3d_status host_variant(int transform, const void *host_cube, int N, ui
     const size_t cb = (size_t)P.batch * N * N * N * in_bytes(o.in_dtype);
     const size_t ob = out_elems(transform, P, o) * 4;
     if (cudaMemcpyAsync(dev_cube, host_cube, cb, cudaMemcpyHostToDevice, st) != cudaSuccess) return DRT3D_ERR_CUDA;
+    // One cube, stacked layout, several dodecants: transform them in groups and copy each group's
+    // output slice to the host on a copy stream while the next group computes (the result's
+    // device-to-host copy is PCIe-bound, ~57 GB/s; this hides the transform behind it).
+    Aux *ax = (P.batch == 1 && o.layout == DRT3D_LAYOUT_STACKED && P.ndod >= 2 && !o.events)
+                  ? aux_for_current_device() : nullptr;
+    if (ax) {
+        const int K = P.ndod, G = K < kHostGroups ? K : kHostGroups;
+        const size_t per_dod = ob / (size_t)K;
+        int kl[12], nk = 0;
+        for (int k = 0; k < 12; ++k)
+            if ((mask >> k) & 1) kl[nk++] = k;
+        int j0 = 0, launches = 0;
+        for (int g = 0; g < G; ++g) {
+            const int d = K / G + (g < K % G ? 1 : 0);
+            uint32_t mg = 0;
+            for (int j = j0; j < j0 + d; ++j) mg |= 1u << kl[j];
+            Plan Pg;
+            s = make_plan(transform, N, mg, o, Pg);
+            if (s != DRT3D_OK) return s;
+            if (Pg.ws_bytes > ws_bytes) return DRT3D_ERR_WORKSPACE;      // cannot happen: fewer instances
+            unsigned char *og = reinterpret_cast<unsigned char *>(dev_out) + per_dod * j0;
+            s = transform == 0 ? run_drt(dev_cube, mg, og, o, Pg, ws, st) : run_djt(dev_cube, mg, og, o, Pg, ws, st);
+            if (s != DRT3D_OK) return s;
+            if (o.launches) launches += *o.launches;
+            if (cudaEventRecord(ax->gdone[g], st) != cudaSuccess) return DRT3D_ERR_CUDA;
+            if (cudaStreamWaitEvent(ax->cp, ax->gdone[g], 0) != cudaSuccess) return DRT3D_ERR_CUDA;
+            if (cudaMemcpyAsync(reinterpret_cast<unsigned char *>(host_out) + per_dod * j0, og, per_dod * d,
+                                cudaMemcpyDeviceToHost, ax->cp) != cudaSuccess)
+                return DRT3D_ERR_CUDA;
+            j0 += d;
+        }
+        if (o.launches) *o.launches = launches;
+        // the caller's stream resumes after the last copy
+        if (cudaEventRecord(ax->cpdone, ax->cp) != cudaSuccess) return DRT3D_ERR_CUDA;
+        return cudaStreamWaitEvent(st, ax->cpdone, 0) == cudaSuccess ? DRT3D_OK : DRT3D_ERR_CUDA;
+    }
     s = transform == 0 ? run_drt(dev_cube, mask, dev_out, o, P, ws, st) : run_djt(dev_cube, mask, dev_out, o, P, ws, st);
     if (s != DRT3D_OK) return s;
     if (cudaMemcpyAsync(host_out, dev_out, ob, cudaMemcpyDeviceToHost, st) != cudaSuccess) return DRT3D_ERR_CUDA;

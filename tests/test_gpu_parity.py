@@ -346,3 +346,45 @@ def test_drt_batched_multichunk_overlap():
                 s1, s2 = int(rng.integers(0, N)), int(rng.integers(0, N))
                 Dd = int(rng.integers(2 * N - s1 - s2, 3 * N))
                 assert int(got[b, k, s1, s2, Dd]) == oracle.drt_point(g, s1, s2, Dd)
+
+
+# ------------------------------------------------------------ host-buffer entry points (e2e path)
+
+def _host_call(kind, cube_np, mask, batch):
+    """drt3d_planes_host / djt3d_lines_host: pinned host cube in, pinned host output out."""
+    N = cube_np.shape[-1]
+    K = bin(mask).count("1")
+    o = d3.make_opts(batch=batch, in_dtype=d3.DRT3D_U8, out_dtype=d3.DRT3D_I32)
+    hcube = torch.from_numpy(np.ascontiguousarray(cube_np)).pin_memory()
+    shape = (batch, K, N, N, 3 * N) if kind == "drt" else (batch, K, N, N, 2 * N, 2 * N)
+    hout = torch.empty(shape, dtype=torch.int32).pin_memory()
+    dcube = torch.empty(hcube.shape, dtype=torch.uint8, device="cuda")
+    dout = torch.empty(shape, dtype=torch.int32, device="cuda")
+    wsb = (d3.drt3d_planes_workspace_size if kind == "drt" else d3.djt3d_lines_workspace_size)(N, mask, o)
+    ws = torch.empty(max(wsb, 256), dtype=torch.uint8, device="cuda")
+    fn = d3.drt3d_planes_host if kind == "drt" else d3.djt3d_lines_host
+    st = torch.cuda.current_stream().cuda_stream
+    assert fn(hcube.data_ptr(), N, mask, hout.data_ptr(), o, dcube.data_ptr(), dout.data_ptr(), ws.data_ptr(), wsb,
+              st) == d3.DRT3D_OK
+    torch.cuda.current_stream().synchronize()
+    return hout.numpy()
+
+
+@pytest.mark.parametrize("N,mask,batch", [(64, 0xFFF, 1), (64, 0x5A3, 1), (32, 0x001, 1), (32, 0xFFF, 2),
+                                          (256, 0xFFF, 1)])
+def test_drt_host_entry(N, mask, batch):
+    """The host-buffer call (dodecant groups copied out while the next group computes, batch 1)
+    returns exactly the device-buffer result; small sizes also against the oracle."""
+    cubes = synth.uniform_cube(N, 31 + N, np.uint8, batch=batch).reshape(batch, N, N, N)
+    got = _host_call("drt", cubes, mask, batch)
+    dev = d3.planes(_gpu(cubes), mask).cpu().numpy()
+    assert np.array_equal(got, dev)
+    if N <= 64:
+        assert np.array_equal(got[0].astype(np.int64), oracle.drt_planes(cubes[0], mask))
+
+
+def test_djt_host_entry():
+    N, mask = 16, 0x0F1
+    cube = synth.uniform_cube(N, 77, np.uint8)
+    got = _host_call("djt", cube[None], mask, 1)
+    assert np.array_equal(got[0].astype(np.int64), oracle.djt_lines(cube, mask))
