@@ -13,9 +13,12 @@
  *    library never allocates device memory, frees, or synchronises, and enqueues
  *    its kernels on `stream` (a cudaStream_t passed as void*, NULL = legacy
  *    default stream).  Multi-chunk DRT calls may also run passes on an internal
- *    auxiliary stream (one per host thread and device, created on first use) that
- *    is forked from and joined back into `stream` within the call, so ordering
- *    with respect to `stream` is unchanged.
+ *    auxiliary stream, and the `_host` calls copy finished dodecant groups to the
+ *    host on an internal copy stream (both one per host thread and device,
+ *    created on first use); each is forked from and joined back into `stream`
+ *    within the call, so ordering with respect to `stream` is unchanged.  The
+ *    inverse captures one iteration as a CUDA graph on an internal stream and
+ *    replays it on `stream` (graphs cached per device, shapes and buffers).
  *  - N must be a power of two, 2 <= N <= 1024 (non-cubic / non-dyadic volumes are
  *    out of scope).
  *  - cube layout: C order [batch][x][y][z], z fastest; element type opts->in_dtype.
