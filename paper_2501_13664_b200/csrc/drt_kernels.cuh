@@ -438,6 +438,57 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
         // slot's shift term and one address add
         constexpr int SUBS = G::THREADS / NCH;             // slots in flight per iteration
         const int q = tid % NCH, sub = tid / NCH;
+#ifdef D3_BULK_STAGE
+        if constexpr (STAGE16) {
+            // one 1-D bulk copy (TMA engine, completes on an mbarrier) per staged row whose window
+            // lies inside its stored row: NCH * 16 contiguous, 16-byte-aligned bytes each (rows are
+            // pre-shifted); warp 0 issues them.  Rows reaching
+            // past either end of the stored row take the zero-filling cp.async path below.
+            __shared__ __align__(8) uint64_t stage_bar;
+            const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&stage_bar));
+            if (tid == 0) {
+                asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(32) : "memory");
+                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            }
+            __syncthreads();
+            const In *rb = inb + (rbase + ((long long)(V1 << K) << nc) + (V2 << K)) * p.in_pitch;
+            if (tid < 32) {
+                uint32_t bytes = 0;
+                for (int slot = tid; slot < S * S; slot += 32) {
+                    const int w1 = slot >> K, w2 = slot & (S - 1);
+                    const int cc = cb + ((sg1 * w1 + sg2 * w2) >> LOG_EPC);
+                    if (cc >= 0 && cc + NCH <= nchunk) {
+                        const char *src = reinterpret_cast<const char *>(rb) +
+                                          ((size_t)((w1 << nc) + w2) * p.in_pitch + (size_t)cc * EPC) * sizeof(In);
+                        const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(sm + slot * SP));
+                        asm volatile(
+                            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                            "l"(src), "r"(NCH * 16), "r"(bar)
+                            : "memory");
+                        bytes += NCH * 16;
+                    }
+                }
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+            }
+            // edge rows: chunk-wise with zero fill
+            for (int i = tid; i < S * S * NCH; i += G::THREADS) {
+                const int slot = i / NCH, qq = i - slot * NCH;
+                const int w1 = slot >> K, w2 = slot & (S - 1);
+                const int c0r = cb + ((sg1 * w1 + sg2 * w2) >> LOG_EPC);
+                if (c0r >= 0 && c0r + NCH <= nchunk) continue;
+                const int cc = c0r + qq;
+                const bool ok = (unsigned)cc < (unsigned)nchunk;
+                const uint32_t off =
+                    ((uint32_t)((w1 << nc) + w2) * (uint32_t)p.in_pitch + (uint32_t)(ok ? cc : 0) * EPC) * (uint32_t)sizeof(In);
+                cp_async16(sm + slot * SP + 16 * qq, reinterpret_cast<const char *>(rb) + off, ok);
+            }
+            PP_MARK(1);
+            cp_async_wait_all();
+            asm volatile(
+                "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}" ::"r"(bar)
+                : "memory");
+        } else
+#endif
         if (sub < SUBS) {
             const In *rb = inb + (rbase + ((long long)(V1 << K) << nc) + (V2 << K)) * p.in_pitch;
             unsigned char *dst = sm + sub * SP + 16 * (STAGE16 ? q : xswz(q));
