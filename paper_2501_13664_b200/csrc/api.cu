@@ -289,31 +289,6 @@ drt3d_status check_ptrs(const void *cube, void *out, void *ws, size_t ws_bytes, 
     return DRT3D_OK;
 }
 
-// EXPERIMENT (env D3_L2_PERSIST_MB): persisting-L2 window over the workspace
-struct L2Window {
-    cudaStream_t st;
-    bool on = false;
-    L2Window(cudaStream_t s, void *ws, size_t bytes) : st(s) {
-        const char *e = getenv("D3_L2_PERSIST_MB");
-        if (!e || !ws || !bytes) return;
-        size_t mb = (size_t)atol(e);
-        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, mb << 20);
-        cudaStreamAttrValue v{};
-        v.accessPolicyWindow.base_ptr = ws;
-        v.accessPolicyWindow.num_bytes = bytes;
-        v.accessPolicyWindow.hitRatio = 1.0f;
-        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        on = cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v) == cudaSuccess;
-    }
-    ~L2Window() {
-        if (!on) return;
-        cudaStreamAttrValue v{};
-        v.accessPolicyWindow.num_bytes = 0;
-        cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v);
-    }
-};
-
 // Cross-stream overlap of consecutive chunks: the first pass of
 // chunk i+1 runs on the caller's stream while the later passes of chunk i run on an auxiliary
 // stream, so the two latency-bound kernels share the SMs.  One auxiliary stream and four
@@ -351,7 +326,6 @@ Aux *aux_for_current_device() {
 
 drt3d_status run_drt(const void *cube, uint32_t mask, void *out, const drt3d_opts &o, const Plan &P, void *ws,
                      cudaStream_t st) {
-    L2Window l2w(st, ws, P.ws_bytes);
     const int8_t(*rows)[3] = table_rows(o.table, 0);
     DrtPass base{};
     base.N = P.N;

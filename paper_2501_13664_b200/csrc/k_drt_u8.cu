@@ -14,15 +14,6 @@ drt3d_status dispatch_drt_u8(int K, int sin, int sout, bool first, bool fin, con
 }
 }  // namespace d3
 
-#ifdef PIPE_PROF
-// debug builds only: read and reset the pipeline clock accounting of drt_final_pipe.cuh
-extern "C" int d3_pipe_prof_read(unsigned long long *out16) {
-    if (cudaMemcpyFromSymbol(out16, d3::d3_pipe_prof, 16 * sizeof(unsigned long long)) != cudaSuccess) return 1;
-    unsigned long long z[16] = {0};
-    return cudaMemcpyToSymbol(d3::d3_pipe_prof, z, sizeof(z)) != cudaSuccess;
-}
-#endif
-
 #ifdef D3_PROF_PASS
 extern "C" int d3_pass_prof_read(unsigned long long *out16) {
     if (cudaMemcpyFromSymbol(out16, d3_pass_prof, 16 * sizeof(unsigned long long)) != cudaSuccess) return 1;

@@ -6,8 +6,6 @@
 #include <cudaTypedefs.h>
 #include "dispatch.h"
 #include "drt_first_swar.cuh"
-#include "drt_final_pipe.cuh"
-#include "drt_final_persist.cuh"
 
 namespace d3 {
 
@@ -53,56 +51,6 @@ drt3d_status launch_drt_k(const DrtPass &prm_in, int ninst, cudaStream_t st) {
     // u16-input final passes use a narrower tile (more resident CTAs per SM); non-final passes keep
     // T / R a power of two (their epilogue shuffles across the T / R runs of a row)
     constexpr int R = DrtTile<K>::R, T = (!FIRST && FINAL && sizeof(In) == 2 && K == 4) ? D3_FINAL16_T : DrtTile<K>::T;
-    if constexpr (!FIRST && FINAL && K == 4 && std::is_same<In, uint16_t>::value && std::is_same<Out, uint32_t>::value) {
-        // experiment (measured slower than the default): D3_PERSIST=1
-        static const bool no_persist = getenv("D3_PERSIST") == nullptr || getenv("D3_NO_TMA_STORE") != nullptr;
-        constexpr int TQ = 48;
-        const int ntd = prm.out_width / TQ;
-        if (!no_persist && getenv("D3_PIPE") == nullptr && prm.layout == 0 && prm.m == 0 && ntd * TQ == prm.out_width &&
-            (ntd & (ntd - 1)) == 0) {
-            // persistent two-CTA/SM final pass with overlapped staging and deferred TMA stores
-            using QG = PersistGeom<K, R, TQ>;
-            auto kern = drt_final_persist_kernel<K, R, TQ>;
-            static std::atomic<uint32_t> smem_done{0};
-            if (!set_smem_once(kern, QG::SMEM, smem_done)) return DRT3D_ERR_CUDA;
-            CUtensorMap omap;
-            if (!make_out_map(&omap, prm.out, prm.N, prm.inst_total, TQ, 1 << K)) return DRT3D_ERR_CUDA;
-            static int nsm = [] {
-                int dev = 0, v = 0;
-                cudaGetDevice(&dev);
-                cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-                return v > 0 ? v : 148;
-            }();
-            int log_ntd = 0;
-            while ((1 << log_ntd) < ntd) ++log_ntd;
-            const long long total = (long long)ninst * (1LL << (2 * (prm.c + prm.m))) * ntd;
-            const int grid = (int)(total < 2 * nsm ? total : 2 * nsm);
-            kern<<<grid, QG::THREADS, QG::SMEM, st>>>(prm, omap, log_ntd, (int)total);
-            return DRT3D_OK;
-        }
-        static const bool use_pipe = getenv("D3_PIPE") != nullptr;   // experiment: pipelined final pass
-        if (use_pipe && prm.layout == 0 && (prm.out_width / 48) * 48 == prm.out_width && ((prm.out_width / 48) & (prm.out_width / 48 - 1)) == 0) {
-            // u16 rows -> int32 stacked output: persistent warp-specialised pipeline (drt_final_pipe.cuh)
-            constexpr int TP = 48;                      // 4 X + 3 Y + 1 producer warps: 255 regs/thread
-            using PG = PipeGeom<K, R, TP>;
-            auto kern = drt_final_pipe_kernel<K, R, TP>;
-            static std::atomic<uint32_t> smem_done{0};
-            if (!set_smem_once(kern, PG::SMEM, smem_done)) return DRT3D_ERR_CUDA;
-            static int nsm = [] {
-                int dev = 0, v = 0;
-                cudaGetDevice(&dev);
-                cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-                return v > 0 ? v : 148;
-            }();
-            const int ntiles_d = prm.out_width / TP;            // a power of two (checked above)
-            int log_ntd = 0;
-            while ((1 << log_ntd) < ntiles_d) ++log_ntd;
-            const long long total = (long long)ninst * (1LL << (2 * (prm.c + prm.m))) * ntiles_d;
-            const int grid = (int)(total < nsm ? total : nsm);
-            kern<<<grid, PG::THREADS, PG::SMEM, st>>>(prm, log_ntd, (int)total);
-            return DRT3D_OK;
-        }
-    }
     if constexpr (FIRST && !FINAL && K >= 3 && std::is_same<In, uint8_t>::value && std::is_same<Out, uint16_t>::value) {
         // u8 voxels -> u16 stage-K rows: packed 16-bit lanes (drt_first_swar.cuh)
 #ifndef SWAR_R
