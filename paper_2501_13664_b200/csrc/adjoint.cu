@@ -521,7 +521,10 @@ inline int pass_plan(int n, int (&ks)[4]) {                          // forward 
     return np;
 }
 
-constexpr int kAdjT = 64, kAdjR = 8;
+#ifndef D3_ADJ_T
+#define D3_ADJ_T 64        // swept 32 / 64 / 128: 2.52 / 2.02 / 2.19 ms (DRT N=256 x12)
+#endif
+constexpr int kAdjT = D3_ADJ_T, kAdjR = 8;
 
 template <int K, class T>
 void launch_adj_pass(const AdjPass &a, int ntiles, int groups, int D, cudaStream_t st) {
