@@ -96,3 +96,29 @@ def test_invert_converges_large(N):
     assert rn[-1] < 0.02 * rn[0]
     err = float(torch.linalg.norm(x - ft) / torch.linalg.norm(ft))
     assert err < 0.15
+
+
+def test_invert_graph_cache_states():
+    """Iterations 2.. replay a captured CUDA graph cached per (device, shapes, buffers): a second call
+    on the same buffers (cache hit, new coefficients), a call on other buffers (new graph) and
+    iters=1 (no graph) all equal the oracle iteration."""
+    N = 16
+    f1, f2 = _phantom(N), np.flip(_phantom(N), 0).copy()
+    b1, b2 = oracle.drt_planes(f1), oracle.drt_planes(f2)
+    ref1, _ = inv.press_multigrid(b1, 3)
+    ref2, _ = inv.press_multigrid(b2, 3)
+    o = d3.make_opts(batch=1, in_dtype=d3.DRT3D_F32, out_dtype=d3.DRT3D_F32)
+    import ctypes
+    wsb = ctypes.c_size_t(0)
+    d3.lib().drt3d_planes_invert_workspace_size(N, 2, 0xFFF, ctypes.byref(o), ctypes.byref(wsb))
+    ws = torch.empty(wsb.value, dtype=torch.uint8, device="cuda")
+    cube = torch.empty((N, N, N), dtype=torch.float32, device="cuda")
+    tol = lambda ref: 1e-4 * np.max(np.abs(ref))
+    for b, ref in ((b1, ref1), (b2, ref2), (b1, ref1)):                # same buffers: capture, hit, hit
+        x, _ = d3.planes_invert(torch.from_numpy(b.astype(np.float32)).cuda(), 3, cube=cube, workspace=ws)
+        assert np.max(np.abs(x.cpu().numpy() - ref)) <= tol(ref)
+    x, _ = d3.planes_invert(torch.from_numpy(b2.astype(np.float32)).cuda(), 3)   # fresh buffers: new graph
+    assert np.max(np.abs(x.cpu().numpy() - ref2)) <= tol(ref2)
+    ref_1, _ = inv.press_multigrid(b1, 1)
+    x, _ = d3.planes_invert(torch.from_numpy(b1.astype(np.float32)).cuda(), 1, cube=cube, workspace=ws)
+    assert np.max(np.abs(x.cpu().numpy() - ref_1)) <= tol(ref_1)

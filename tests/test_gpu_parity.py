@@ -388,3 +388,29 @@ def test_djt_host_entry():
     cube = synth.uniform_cube(N, 77, np.uint8)
     got = _host_call("djt", cube[None], mask, 1)
     assert np.array_equal(got[0].astype(np.int64), oracle.djt_lines(cube, mask))
+
+
+def test_entry_points_on_a_side_stream():
+    """Every call enqueues on the caller's stream (internal streams fork from and join it): run the
+    forward (multi-chunk batch), backprojection, inverse and detection on a non-default stream,
+    synchronise only that stream, and compare with default-stream results."""
+    N, B = 128, 9
+    cubes = synth.uniform_cube(N, 901, np.uint8, batch=B).reshape(B, N, N, N)
+    ref = d3.planes(_gpu(cubes), 0xFFF)
+    small = _gpu(synth.uniform_cube(16, 5, np.uint8))
+    ref_adj = d3.planes_adjoint(d3.planes(small, 0xFFF), 0xFFF)
+    ref_inv, _ = d3.planes_invert(d3.planes(small.float(), 0xFFF), 3)
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        got = d3.planes(_gpu(cubes), 0xFFF)
+        adj = d3.planes_adjoint(d3.planes(small, 0xFFF), 0xFFF)
+        xin, _ = d3.planes_invert(d3.planes(small.float(), 0xFFF), 3)
+        flags, _ = d3.detect_planes(got[0], 0xFFF, 1, 3, 1, 10)
+    s.synchronize()
+    assert bool(torch.equal(got, ref))
+    assert bool(torch.equal(adj, ref_adj))
+    assert bool(torch.equal(xin, ref_inv))                             # deterministic kernels
+    ref_flags, _ = d3.detect_planes(ref[0], 0xFFF, 1, 3, 1, 10)
+    torch.cuda.synchronize()
+    assert bool(torch.equal(flags, ref_flags))
