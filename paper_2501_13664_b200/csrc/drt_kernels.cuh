@@ -514,7 +514,16 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
     Acc acc[S][R];
     int xb, xr;
     task_row_run(tid, G::NRX, S, xb, xr);
-    const int yr = tid % G::NRY, yb = tid / G::NRY;
+#ifndef D3_Y8
+#define D3_Y8 1
+#endif
+    // y-step task (r1 = yb, run yr).  With fewer than 8 runs per row (T=48: 6) a quarter-warp of
+    // the compact mapping spans two rows whose X slots sit 16 x 17 chunks = 0 (mod 8 bank groups)
+    // apart, so their reads collide; giving each row 8 lanes (the last NRY..7 idle) keeps every
+    // quarter-warp on one row and its chunk reads conflict-free.
+    constexpr bool Y8 = D3_Y8 && STAGE16 && FINAL && G::NRY < 8 && G::THREADS >= 8 * S;
+    const int yr = Y8 ? (tid & 7) : tid % G::NRY, yb = Y8 ? (tid >> 3) : tid / G::NRY;
+    const bool yact = Y8 ? (yr < G::NRY) : (tid < G::YT);
     auto zero_acc = [&]() {
 #pragma unroll
         for (int i = 0; i < S; ++i)
@@ -543,7 +552,7 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
         if (tid < G::XT) write_x();
         __syncthreads();
         PP_MARK(5);
-        if (tid < G::YT) {
+        if (yact) {
             zero_acc();
             drt_accumulate<K, R, SP, false, Acc>(sm, yb * S, 1, yr * (R / 4), p.one, acc);
         }
@@ -552,7 +561,7 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
         // both steps read 32-bit rows: one code path, two iterations
 #pragma unroll 1
         for (int step = 0; step < 2; ++step) {
-            const bool act = tid < (step ? G::YT : G::XT);
+            const bool act = step ? yact : (tid < G::XT);
             const int r = step ? yr : xr, b = step ? yb : xb;
             if (act) {
                 zero_acc();
@@ -569,7 +578,7 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
     // ---- intermediate output: rows stored pre-shifted by rho (see common.cuh), realigned
     // across the NRY runs of a row with one shuffle per word
     if constexpr (!FINAL) {
-        if (tid < G::YT) {
+        if (yact) {
             constexpr int E = 4 / (int)sizeof(Out);        // elements per 32-bit word
             constexpr int EPC = 4 * E;                     // elements per 16-byte chunk
             constexpr int NWO = R / E;                     // words per run
@@ -621,15 +630,33 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
     if constexpr (FINAL && sizeof(Out) == 4) {
         if (p.tma_store) {
             __syncthreads();                                 // every y-step read of X is done
-            if (tid < G::YT) {
+            if (yact) {
                 unsigned char *row = sm + ((yb * S) * T + yr * R) * 4;
+#ifndef D3_Y8_STORE_SWAP
+#define D3_Y8_STORE_SWAP 1
+#endif
+                if constexpr (Y8 && R == 8 && D3_Y8_STORE_SWAP) {
+                    // runs 4, 5 write their two chunks in the opposite order: with runs 0..3 they
+                    // then cover 8 distinct bank groups per store instruction of a quarter-warp
+                    const bool sw = (yr & 4) != 0;
 #pragma unroll
-                for (int r2 = 0; r2 < S; ++r2)
+                    for (int r2 = 0; r2 < S; ++r2) {
+                        const uint4 c0 = make_uint4(Lane<Acc>::bits(acc[r2][0]), Lane<Acc>::bits(acc[r2][1]),
+                                                    Lane<Acc>::bits(acc[r2][2]), Lane<Acc>::bits(acc[r2][3]));
+                        const uint4 c1 = make_uint4(Lane<Acc>::bits(acc[r2][4]), Lane<Acc>::bits(acc[r2][5]),
+                                                    Lane<Acc>::bits(acc[r2][6]), Lane<Acc>::bits(acc[r2][7]));
+                        *reinterpret_cast<uint4 *>(row + (r2 * T + (sw ? 4 : 0)) * 4) = sw ? c1 : c0;
+                        *reinterpret_cast<uint4 *>(row + (r2 * T + (sw ? 0 : 4)) * 4) = sw ? c0 : c1;
+                    }
+                } else {
 #pragma unroll
-                    for (int q = 0; q < R / 4; ++q)
-                        *reinterpret_cast<uint4 *>(row + (r2 * T + 4 * q) * 4) =
-                            make_uint4(Lane<Acc>::bits(acc[r2][4 * q]), Lane<Acc>::bits(acc[r2][4 * q + 1]),
-                                       Lane<Acc>::bits(acc[r2][4 * q + 2]), Lane<Acc>::bits(acc[r2][4 * q + 3]));
+                    for (int r2 = 0; r2 < S; ++r2)
+#pragma unroll
+                        for (int q = 0; q < R / 4; ++q)
+                            *reinterpret_cast<uint4 *>(row + (r2 * T + 4 * q) * 4) =
+                                make_uint4(Lane<Acc>::bits(acc[r2][4 * q]), Lane<Acc>::bits(acc[r2][4 * q + 1]),
+                                           Lane<Acc>::bits(acc[r2][4 * q + 2]), Lane<Acc>::bits(acc[r2][4 * q + 3]));
+                }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncthreads();
@@ -669,7 +696,7 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
     }
 
     // ---- store out(r1 = yb, r2, run yr)
-    if (tid < G::YT) {
+    if (yact) {
         const int r1 = yb, e0 = yr * R;
         if (mosaic) {
 #pragma unroll
