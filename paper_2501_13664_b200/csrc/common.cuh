@@ -183,13 +183,22 @@ __device__ __forceinline__ uint4 ld_hint_v4(const void *p, uint64_t pol) {
 }
 
 // Task -> (row, run) with quarter-warps on 8 consecutive runs of one row (conflict-free
-// 16-byte shared loads): tasks below 8 * nrows cover runs 0..7, the rest runs 8..nr-1.
-__device__ __forceinline__ void task_row_run(int t, int nr, int nrows, int &row, int &run) {
+// 16-byte shared loads): tasks below 8 * nrows cover runs 0..7, the rest runs 8..nr-1.  With
+// row_fast the extra runs go row-fastest, so a quarter-warp of them reads 8 different rows at one
+// run (their slots start in different bank groups) instead of 4 rows x 2 runs (which collide in
+// the SWAR kernel's slot layout; measured neutral-to-worse for the 32-bit passes, so off there).
+__device__ __forceinline__ void task_row_run(int t, int nr, int nrows, int &row, int &run, bool row_fast = false) {
     if (nr <= 8 || t < 8 * nrows) { row = t >> 3; run = t & 7; if (nr < 8) { row = t / nr; run = t - row * nr; } return; }
     const int u = t - 8 * nrows, extra = nr - 8;
-    row = u / extra;
-    run = 8 + (u - row * extra);
+    if (row_fast) {
+        row = u % nrows;
+        run = 8 + u / nrows;
+    } else {
+        row = u / extra;
+        run = 8 + (u - row * extra);
+    }
 }
+
 
 // streaming (evict-first) 16-byte global store for final outputs that are
 // never re-read by this call.

@@ -71,15 +71,35 @@ __device__ unsigned long long d3_swar_prof[16];
 #define SW_MARK(i)
 #endif
 
-// Output staging rows (r1, r2) start row_skew(r1) = r1 words after their 33-word slot: the
-// unpack writes of a warp cover 4 consecutive r1 whose slots are 16 rows = 528 words apart
-// (0 mod 16 banks); with the skew the r1 blocks are 529 = 17 (mod 32) words apart, so the four
-// land on distinct residues mod 4 and the stores are conflict-free.  Rows never overlap (the
-// skew grows by one word per 16-row block); the copy-out reads collide on one lane pair at most.
+// Output staging rows (r1, r2) start row_skew(r1) words after their 33-word slot (rows are
+// 33 words apart; 16 rows of one r1 = 528 = 16 mod 32 banks).  Two access patterns must both be
+// conflict-free:
+//   - the unpack stores: a warp writes 4 consecutive r1 x 8 runs (4 words apart) of one r2, so
+//     the 4 skews must differ mod 4;
+//   - the copy-out reads: a warp reads 32 rows, two 16-row blocks whose bank ranges must not
+//     overlap.  The copy-out pairs r1 with r1 + 4 (copy_row below), so skew(r1 + 4) - skew(r1)
+//     must be 16 mod 32.
+// skew = (r1 & 3) + 16 ((r1 >> 2) & 1) satisfies both; + 32 (r1 >> 3) (0 mod 32) keeps rows from
+// overlapping where the skew drops.
+// (S = 8, the K = 3 first pass: skew r1 and the plain order.)
 #ifdef D3_SWAR_NO_SKEW
-__device__ __forceinline__ int row_skew(int) { return 0; }
+template <int S> __device__ __forceinline__ int row_skew(int) { return 0; }
+template <int S> __device__ __forceinline__ int copy_row(int i) { return i; }
 #else
-__device__ __forceinline__ int row_skew(int r1) { return r1; }
+template <int S> __device__ __forceinline__ int row_skew(int r1) {
+    if constexpr (S == 16) return (r1 & 3) + 16 * ((r1 >> 2) & 1) + 32 * (r1 >> 3);
+    else return r1;
+}
+// copy-out order: each 32-row block of the loop = rows (a, r2) and (a + 4, r2), r2 = 0..15
+template <int S> __device__ __forceinline__ int copy_row(int i) {
+    if constexpr (S == 16) {
+        const int blk = i >> 5, half = (i >> 4) & 1, r2 = i & 15;
+        const int r1 = ((blk >> 2) << 3) + (blk & 3) + 4 * half;
+        return (r1 << 4) | r2;
+    } else {
+        return i;
+    }
+}
 #endif
 
 #ifndef SWAR_FMA16
@@ -253,7 +273,7 @@ drt_first_swar_kernel(const DrtPass p) {
 #pragma unroll 1
     for (int step = 0; step < 2; ++step) {
         int grp, run;
-        task_row_run(tid, step ? G::NRY : G::NRX, H2, grp, run);
+        task_row_run(tid, step ? G::NRY : G::NRX, H2, grp, run, true);
         const bool act = tid < (step ? G::YT : G::XT);
         if (act) {
 #pragma unroll
@@ -292,7 +312,7 @@ drt_first_swar_kernel(const DrtPass p) {
 #pragma unroll
                     for (int r2 = 0; r2 < S; ++r2) {
                         uint32_t *o = reinterpret_cast<uint32_t *>(sm + G::ORP * ((grp + h * H2) * S + r2)) +
-                                      row_skew(grp + h * H2) + (R / 2) * run;
+                                      row_skew<S>(grp + h * H2) + (R / 2) * run;
 #pragma unroll
                         for (int i = 0; i < R / 2; ++i) o[i] = __byte_perm(acc[r2][2 * i], acc[r2][2 * i + 1], sel);
                     }
@@ -317,7 +337,8 @@ drt_first_swar_kernel(const DrtPass p) {
     const int mK = (1 << p.next_k) - 1;
     const int wv1 = V1 & mK, wv2 = V2 & mK;
     constexpr int NCK = T / 8;
-    for (int rr = tid; rr < S * S; rr += blockDim.x) {
+    for (int ii = tid; ii < S * S; ii += blockDim.x) {
+        const int rr = copy_row<S>(ii);
         const int r1 = rr >> K, r2 = rr & (S - 1);
         const int rho = (r1 * wv1 + r2 * wv2) & 7;
         const long long row = ((((long long)r1 << K) + r2) << (2 * m)) + ((long long)V1 << m) + V2;
@@ -327,8 +348,8 @@ drt_first_swar_kernel(const DrtPass p) {
         {
             // every lane reads its row from word 0 (odd row pitch: conflict-free), the rho/2 word
             // offset is applied with selects (overruns the row by 3 words: inside the staging area)
-            const uint32_t *srow = reinterpret_cast<const uint32_t *>(sm + G::ORP * rr) + row_skew(r1);
-            static_assert(G::SMEM0 >= S * S * G::ORP + 4 * S + 12, "skewed rows + copy-out overrun");
+            const uint32_t *srow = reinterpret_cast<const uint32_t *>(sm + G::ORP * rr) + row_skew<S>(r1);
+            static_assert(G::SMEM0 >= S * S * G::ORP + 4 * 51 + 12, "skewed rows + copy-out overrun");
             uint32_t w0[4 * NCK + 4];
 #pragma unroll
             for (int i = 0; i < 4 * NCK + 4; ++i) w0[i] = srow[i];
@@ -355,7 +376,7 @@ drt_first_swar_kernel(const DrtPass p) {
         }
         if (rho > 0 && d0 >= 8) {
             // tile elements [0, rho) end the previous chunk: window (zeros, row words 0..3)
-            const uint32_t *r0 = reinterpret_cast<const uint32_t *>(sm + G::ORP * rr) + row_skew(r1);
+            const uint32_t *r0 = reinterpret_cast<const uint32_t *>(sm + G::ORP * rr) + row_skew<S>(r1);
             uint32_t tw[8] = {0u, 0u, 0u, 0u, r0[0], r0[1], r0[2], r0[3]}, v[4];
             window_chunk<2>(tw, rho, 0, v);
             store_chunk_tail<2>(dst - 8, v, rho);
