@@ -635,9 +635,10 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
 #ifndef D3_Y8_STORE_SWAP
 #define D3_Y8_STORE_SWAP 1
 #endif
-                if constexpr (Y8 && R == 8 && D3_Y8_STORE_SWAP) {
-                    // runs 4, 5 write their two chunks in the opposite order: with runs 0..3 they
+                if constexpr ((Y8 || G::NRY == 8) && R == 8 && D3_Y8_STORE_SWAP) {
+                    // runs 4.. write their two chunks in the opposite order: with runs 0..3 they
                     // then cover 8 distinct bank groups per store instruction of a quarter-warp
+                    // (one row per quarter-warp: the Y8 mapping, or 8 runs per row at T = 64)
                     const bool sw = (yr & 4) != 0;
 #pragma unroll
                     for (int r2 = 0; r2 < S; ++r2) {
