@@ -354,11 +354,21 @@ drt_first_swar_kernel(const DrtPass p) {
 #pragma unroll
             for (int i = 0; i < 4 * NCK + 4; ++i) w0[i] = srow[i];
             const int q = rho >> 1;
+#ifndef D3_SWAR_SEL4
+            // barrel shift by q = rho/2 words: by 1 if bit 0, then by 2 if bit 1 (2 selects per
+            // word instead of sel4's 3)
+            const bool b0 = q & 1, b1 = (q & 2) != 0;
+#pragma unroll
+            for (int i = 0; i < 4 * NCK + 3; ++i) w0[i] = b0 ? w0[i + 1] : w0[i];
+#pragma unroll
+            for (int i = 0; i < 4 * NCK + 1; ++i) w[i] = b1 ? w0[i + 2] : w0[i];
+#else
 #pragma unroll
             for (int i = 0; i < 4 * NCK + 1; ++i) {
                 const uint32_t c4[4] = {w0[i], w0[i + 1], w0[i + 2], w0[i + 3]};
                 w[i] = sel4(c4, q);
             }
+#endif
         }
 #pragma unroll
         for (int k = 0; k < NCK; ++k) {
