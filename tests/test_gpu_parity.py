@@ -414,3 +414,42 @@ def test_entry_points_on_a_side_stream():
     ref_flags, _ = d3.detect_planes(ref[0], 0xFFF, 1, 3, 1, 10)
     torch.cuda.synchronize()
     assert bool(torch.equal(flags, ref_flags))
+
+
+def test_concurrent_host_threads():
+    """Three host threads, each on its own stream, call the forward (multi-chunk batch),
+    backprojection and inverse concurrently (ctypes releases the GIL): results equal the serial
+    ones (per-thread auxiliary streams, the graph cache's lock, per-device attribute flags)."""
+    import threading
+    N, B = 128, 9
+    cubes = [synth.uniform_cube(N, 950 + t, np.uint8, batch=B).reshape(B, N, N, N) for t in range(3)]
+    small = [_gpu(synth.uniform_cube(16, 960 + t, np.uint8)) for t in range(3)]
+    ref = [d3.planes(_gpu(c), 0xFFF) for c in cubes]
+    ref_adj = [d3.planes_adjoint(d3.planes(s, 0xFFF), 0xFFF) for s in small]
+    ref_inv = [d3.planes_invert(d3.planes(s.float(), 0xFFF), 3)[0] for s in small]
+    torch.cuda.synchronize()
+    out, errors = [None] * 3, []
+
+    def work(t):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for _ in range(3):
+                    a = d3.planes(_gpu(cubes[t]), 0xFFF)
+                    b = d3.planes_adjoint(d3.planes(small[t], 0xFFF), 0xFFF)
+                    c, _ = d3.planes_invert(d3.planes(small[t].float(), 0xFFF), 3)
+            s.synchronize()
+            out[t] = (a, b, c)
+        except Exception as e:                                         # surfaced below
+            errors.append(e)
+
+    threads = [threading.Thread(target=work, args=(t,)) for t in range(3)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
+    for t in range(3):
+        assert bool(torch.equal(out[t][0], ref[t]))
+        assert bool(torch.equal(out[t][1], ref_adj[t]))
+        assert bool(torch.equal(out[t][2], ref_inv[t]))
