@@ -114,7 +114,11 @@ template <> struct DjtTile<4> { static constexpr int R = 8, T1 = 4, T2 = 64; };
 
 template <int K, class In, class Acc, class Out, bool FIRST, bool FINAL>
 drt3d_status launch_djt_k(DjtPass prm, int ninst, cudaStream_t st) {
-    constexpr int R = DjtTile<K>::R, T1 = DjtTile<K>::T1, T2 = DjtTile<K>::T2;
+#ifndef D3_DJT_FIRST_T1
+#define D3_DJT_FIRST_T1 4      // first passes: 4-row tiles (twice the CTAs of 8 at N=64: cfg4 -2%)
+#endif
+    constexpr int R = DjtTile<K>::R, T2 = DjtTile<K>::T2;
+    constexpr int T1 = (FIRST && D3_DJT_FIRST_T1 > 0) ? D3_DJT_FIRST_T1 : DjtTile<K>::T1;
     using G = DjtGeom<K, R, T1, T2>;
     auto kern = djt_pass_kernel<K, R, T1, T2, In, Acc, Out, FIRST, FINAL>;
     static std::atomic<uint32_t> smem_done{0};
