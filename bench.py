@@ -343,6 +343,66 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+# ------------------------------------------------------------ CPU oracle per BASELINE config
+# (the oracle beside every configuration; part of the reference arm, the
+# only place besides the cpu_baseline leg where bench.py executes oracle/)
+_CUBES = {}
+
+
+def _oracle_job(args):
+    import oracle
+    import synth
+    from oracle import tables
+    cfg, kind, b, k = args
+    if cfg not in _CUBES:                      # once per process: the inputs are large to regenerate
+        _CUBES[cfg] = synth.config_input(cfg)
+    cube = _CUBES[cfg][b]
+    if kind == "drt":
+        oracle.drt_alg1(oracle.orient(cube, tables.DRT_HEMISPHERE[k]))
+    else:
+        oracle.djt_alg3(oracle.orient(cube, tables.table(tables.TABLE_HEMISPHERE, "djt")[k]))
+    return 0
+
+
+def _timed(jobs, workers, reps):
+    from concurrent.futures import ProcessPoolExecutor
+    best = 1e30
+    for r in range(reps + 1):                  # one warm-up, then best of reps
+        t0 = time.perf_counter()
+        if workers == 1:
+            for j in jobs:
+                _oracle_job(j)
+        else:
+            with ProcessPoolExecutor(workers) as ex:
+                list(ex.map(_oracle_job, jobs))
+        dt = time.perf_counter() - t0
+        if r > 0:
+            best = min(best, dt)
+    return best
+
+
+def run_reference_configs(args):
+    """T=1 (one process) and T=all (one process per dodecant or cube) oracle wall time for each
+    BASELINE config on this host; config 3 times single dodecants (about 11 s each) and scales by
+    the dodecant count.  One JSON line per config."""
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    cores = os.cpu_count() or 1
+    specs = {1: ("drt", 1, [0]), 2: ("drt", 1, range(12)), 4: ("djt", 1, [0]), 5: ("drt", 256, range(12))}
+    for cfg, (kind, nb, ks) in specs.items():
+        jobs = [(cfg, kind, b, k) for b in range(nb) for k in ks]
+        reps = 1 if cfg == 5 else 3
+        t1 = _timed(jobs, 1, reps)
+        ta = _timed(jobs, min(cores, len(jobs)), reps)
+        print(json.dumps({"impl": "reference", "config": cfg, "oracle_T1_ms": 1e3 * t1, "oracle_Tall_ms": 1e3 * ta,
+                          "cores": min(cores, len(jobs))}), flush=True)
+    t1 = _timed([(3, "drt", 0, 0)], 1, 1)
+    w = min(cores, 12)
+    ta = _timed([(3, "drt", 0, k) for k in range(12)], w, 1)
+    print(json.dumps({"impl": "reference", "config": 3, "oracle_T1_ms": 12e3 * t1, "oracle_T1_note": "12 x one dodecant",
+                      "oracle_Tall_ms": 1e3 * ta, "cores": w}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -353,10 +413,14 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--warmup-reference", action="store_true",
                     help="also run the (slow) oracle during warm-up steps of --impl reference")
+    ap.add_argument("--configs", action="store_true",
+                    help="with --impl reference: time the oracle on every BASELINE config (BASELINE.md section 4)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
+    if args.impl == "reference" and args.configs:
+        run_reference_configs(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)
