@@ -95,7 +95,12 @@ drt3d_status drt3d_orientation_table(int table, int transform, int8_t rows[36]);
  * s1, s2 in [0, N), D in [0, 3N) (D = 0, 1 and D < 2N - s1 - s2 are 0).
  * STACKED output: [batch][popcount(mask)][N][N][3N] of out_dtype.
  * MOSAIC output (mask must be 0xFFF): [batch][4N][4N][3N-2], block
- * DodecantCoords[k] holds dodecant k with OutOrder[k] applied, d = D - 2.     */
+ * DodecantCoords[k] holds dodecant k with OutOrder[k] applied to (s1, s2) by
+ * reading A, d = D - 2; 4 unused blocks are 0.  OutOrder rows 0-3 are the
+ * repaired rows (-1,-2,3), (-2,1,3), (1,2,3), (2,-1,3) of DESIGN.md reading
+ * R13: with them, and only them, the boundary planes neighbouring dodecants
+ * share lie on facing block edges ("rotated so that all of them fit
+ * accurately", fig:shapeOutput; HEMISPHERE table).        */
 size_t drt3d_planes_out_elems(int N, uint32_t dodecant_mask, const drt3d_opts *opts);
 drt3d_status drt3d_planes_workspace_size(int N, uint32_t dodecant_mask, const drt3d_opts *opts,
                                          size_t *bytes);

@@ -10,9 +10,9 @@ marshals numpy arrays, applies the orientation (reading A: numpy transpose and
 flip, Alg. 2) and assembles the stacked / mosaic layouts.
 
 Parity status per function: every function below is
-pinned by tests/test_oracle_*.py except `mosaic`, whose intra-block orientation
-is cosmetic: its block placement is pinned,
-the within-block OutOrder reading is "parity unpinned".
+pinned by tests/test_oracle_*.py; `mosaic` by its block placement and by the
+seams of fig:shapeOutput (the shared boundary planes of
+neighbouring dodecants sit on facing block edges, reading R13).
 """
 from __future__ import annotations
 
@@ -179,13 +179,15 @@ def drt_planes(cube: np.ndarray, mask: int = 0xFFF, table: int = tables.TABLE_HE
 def mosaic(stacked: np.ndarray) -> np.ndarray:
     """Alg. 2 placement of the 12 stacked dodecants
     [12][N][N][3N] into the 4N x 4N x (3N-2) mosaic: block
-    (DodecantCoords[k]) with OutOrder[k] applied to (s1, s2), d = D - 2.
-    The within-block orientation is cosmetic: parity unpinned."""
+    DodecantCoords[k], OutOrder[k] applied to (s1, s2) by reading A (permute,
+    then flip the permuted axis), d = D - 2.  OutOrder rows 0-3 are the
+    repaired rows of reading R13 (tables.MOSAIC_OUT_ORDER), which make the
+    dodecants "fit accurately" (fig:shapeOutput, PAPER.md:378)."""
     K, N = stacked.shape[0], stacked.shape[1]
     assert K == 12
     out = np.zeros((4 * N, 4 * N, 3 * N - 2), stacked.dtype)
     for k in range(12):
-        o = tables.OUT_ORDER[k]
+        o = tables.MOSAIC_OUT_ORDER[k]
         blk = stacked[k][:, :, 2:]
         # permute the (s1, s2) axes by |o0|,|o1| and flip negative ones
         blk = np.transpose(blk, [abs(o[0]) - 1, abs(o[1]) - 1, 2])

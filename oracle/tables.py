@@ -54,6 +54,20 @@ DODECANT_COORDS = [
     (2, 0), (1, 0), (2, 3), (1, 3),
 ]
 
+# OutOrder as the mosaic applies it (reading R13).  fig:shapeOutput
+# fixes the mosaic's geometry: "Each individual dodecant output is rotated so that all of them fit
+# accurately" and "the black dots mark the position of x, y, and z null normals".  Within each
+# normal set the dodecants share their boundary planes (out_0[0][s] = out_3[s][0], ...: twelve
+# identities, tests/test_oracle_drt.py), and with DodecantCoords verbatim exactly one within-block
+# orientation per dodecant puts every shared boundary on facing edges of neighbouring blocks (the
+# y- and x-sets across the hemisphere's wrap).  Rows 4-11 of the printed OutOrder are that
+# orientation under reading A; printed rows 0-3 (the z-set) act as if s1 and s2 were exchanged
+# and would put all four z-face seams on the wrong edges, so they are replaced by the unique
+# rows that close them (their null-normal columns then meet at the mosaic's centre).
+MOSAIC_OUT_ORDER = [
+    (-1, -2, 3), (-2, 1, 3), (1, 2, 3), (2, -1, 3),
+] + OUT_ORDER[4:]
+
 TABLE_HEMISPHERE, TABLE_PRINTED, TABLE_SHARED = 0, 1, 2
 
 

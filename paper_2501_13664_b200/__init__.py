@@ -164,15 +164,64 @@ def djt3d_lines_host(hcube_ptr, N, mask, hout_ptr, opts, dcube_ptr, dout_ptr, ws
 
 
 # ------------------------------------------------------------ torch helpers
+# Every helper allocates its temporaries (contiguous copies, output, workspace) on the stream the
+# call is enqueued on, so the caching allocator never hands them to other work while the kernels
+# may still use them; caller-supplied buffers are checked (shape, dtype, contiguity, device) and
+# the C ABI is told their real sizes.
 
 def _dtype_code(t):
     import torch
-    return {torch.uint8: DRT3D_U8, torch.int32: DRT3D_I32, torch.float32: DRT3D_F32}[t.dtype]
+    try:
+        return {torch.uint8: DRT3D_U8, torch.int32: DRT3D_I32, torch.float32: DRT3D_F32}[t.dtype]
+    except KeyError:
+        raise Drt3dError(f"unsupported cube dtype {t.dtype} (uint8, int32 or float32)") from None
+
+
+def _stream(stream, device):
+    """torch.cuda.Stream for `stream`: None = the current stream, a torch stream, or a raw
+    cudaStream_t handle (wrapped as an external stream)."""
+    import torch
+    if stream is None:
+        return torch.cuda.current_stream(device)
+    if isinstance(stream, torch.cuda.Stream):
+        return stream
+    return torch.cuda.ExternalStream(int(stream), device=device)
+
+
+def _popcount(mask: int) -> int:
+    if not 0 < mask < (1 << 12):
+        raise Drt3dError(f"dodecant mask {mask:#x} outside [1, 2^12)")
+    return bin(mask).count("1")
+
+
+def _user_tensor(t, shape, dtype, device, what):
+    if (tuple(t.shape) != tuple(shape) or t.dtype != dtype or not t.is_contiguous() or not t.is_cuda
+            or t.device != device):
+        raise Drt3dError(f"{what} must be a contiguous {dtype} CUDA tensor of shape {tuple(shape)} on {device}, "
+                         f"got {t.dtype} {tuple(t.shape)} on {t.device}")
+    return t
+
+
+def _workspace(workspace, need, device):
+    """(tensor or None, size in bytes actually available)."""
+    import torch
+    if workspace is None:
+        if not need:
+            return None, 0
+        workspace = torch.empty(need, dtype=torch.uint8, device=device)
+    elif not workspace.is_cuda or workspace.device != device or not workspace.is_contiguous():
+        raise Drt3dError("workspace must be a contiguous CUDA tensor on the cube's device")
+    return workspace, workspace.numel() * workspace.element_size()
+
+
+def _opts_from(o, opts):
+    if opts is not None:
+        o.events, o.max_events, o.launches, o.launch_kind = opts.events, opts.max_events, opts.launches, opts.launch_kind
 
 
 def _prep(cube, layout, table):
     import torch
-    if not cube.is_cuda:
+    if not isinstance(cube, torch.Tensor) or not cube.is_cuda:
         raise Drt3dError("cube must be a CUDA tensor (use the *_host C entry points for host data)")
     c = cube.contiguous()
     if c.dim() == 3:
@@ -185,80 +234,89 @@ def _prep(cube, layout, table):
     return c, o, (torch.float32 if odt == DRT3D_F32 else torch.int32)
 
 
+def _transform(kind, cube, mask, layout, table, out, workspace, stream, opts):
+    import torch
+    st = _stream(stream, cube.device)
+    with torch.cuda.stream(st):
+        c, o, odt = _prep(cube, layout, table)
+        _opts_from(o, opts)
+        B, N = c.shape[0], c.shape[1]
+        K = _popcount(mask)
+        if kind == "drt":
+            shape = (B, K, N, N, 3 * N) if layout == DRT3D_LAYOUT_STACKED else (B, 4 * N, 4 * N, 3 * N - 2)
+        else:
+            shape = (B, K, N, N, 2 * N, 2 * N)
+        if out is None:
+            out = torch.empty(shape, dtype=odt, device=c.device)
+        else:
+            # a 3-D cube may come with an output without the batch dimension
+            user_shape = shape[1:] if cube.dim() == 3 and tuple(out.shape) == shape[1:] else shape
+            out = _user_tensor(out, user_shape, odt, c.device, "out").view(shape)
+        need = (drt3d_planes_workspace_size if kind == "drt" else djt3d_lines_workspace_size)(N, mask, o)
+        ws, ws_bytes = _workspace(workspace, need, c.device)
+        fn = drt3d_planes if kind == "drt" else djt3d_lines
+        s = fn(c.data_ptr(), N, mask, out.data_ptr(), o, ws.data_ptr() if ws is not None else None, ws_bytes,
+               st.cuda_stream)
+    _check(s, "drt3d_planes" if kind == "drt" else "djt3d_lines")
+    return out if cube.dim() == 4 else out[0]
+
+
 def planes(cube, mask: int = 0xFFF, layout: int = DRT3D_LAYOUT_STACKED, table: int = DRT3D_TABLE_HEMISPHERE,
            out=None, workspace=None, stream=None, opts: drt3d_opts | None = None):
     """3D DRT of planes of a CUDA cube [B,N,N,N] (or [N,N,N]).
 
-    Returns out [B, K, N, N, 3N] (STACKED) or [B, 4N, 4N, 3N-2] (MOSAIC)."""
-    import torch
-    c, o, odt = _prep(cube, layout, table)
-    if opts is not None:
-        o.events, o.max_events, o.launches, o.launch_kind = opts.events, opts.max_events, opts.launches, opts.launch_kind
-    B, N = c.shape[0], c.shape[1]
-    K = bin(mask & 0xFFF).count("1")
-    shape = (B, K, N, N, 3 * N) if layout == DRT3D_LAYOUT_STACKED else (B, 4 * N, 4 * N, 3 * N - 2)
-    if out is None:
-        out = torch.empty(shape, dtype=odt, device=c.device)
-    ws_bytes = drt3d_planes_workspace_size(N, mask, o)
-    if workspace is None and ws_bytes:
-        workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=c.device)
-    st = stream if stream is not None else torch.cuda.current_stream(c.device).cuda_stream
-    s = drt3d_planes(c.data_ptr(), N, mask, out.data_ptr(), o,
-                     workspace.data_ptr() if workspace is not None else None, ws_bytes, st)
-    _check(s, "drt3d_planes")
-    return out if cube.dim() == 4 else out[0]
+    Returns out [B, K, N, N, 3N] (STACKED) or [B, 4N, 4N, 3N-2] (MOSAIC).  `stream`: None (the
+    current stream), a torch.cuda.Stream or a raw cudaStream_t handle."""
+    return _transform("drt", cube, mask, layout, table, out, workspace, stream, opts)
 
 
 def lines(cube, mask: int = 0x001, table: int = DRT3D_TABLE_HEMISPHERE, out=None, workspace=None, stream=None,
           opts: drt3d_opts | None = None):
     """3D DJT of lines of a CUDA cube: out [B, K, N, N, 2N, 2N]."""
-    import torch
-    c, o, odt = _prep(cube, DRT3D_LAYOUT_STACKED, table)
-    if opts is not None:
-        o.events, o.max_events, o.launches, o.launch_kind = opts.events, opts.max_events, opts.launches, opts.launch_kind
-    B, N = c.shape[0], c.shape[1]
-    K = bin(mask & 0xFFF).count("1")
-    if out is None:
-        out = torch.empty((B, K, N, N, 2 * N, 2 * N), dtype=odt, device=c.device)
-    ws_bytes = djt3d_lines_workspace_size(N, mask, o)
-    if workspace is None and ws_bytes:
-        workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=c.device)
-    st = stream if stream is not None else torch.cuda.current_stream(c.device).cuda_stream
-    s = djt3d_lines(c.data_ptr(), N, mask, out.data_ptr(), o,
-                    workspace.data_ptr() if workspace is not None else None, ws_bytes, st)
-    _check(s, "djt3d_lines")
-    return out if cube.dim() == 4 else out[0]
+    return _transform("djt", cube, mask, DRT3D_LAYOUT_STACKED, table, out, workspace, stream, opts)
 
 
 # ------------------------------------------------------------ adjoints (F-1)
 
 def _adjoint(kind, coef, mask, table, cube, workspace, stream, opts):
     import torch
-    if not coef.is_cuda:
+    if not isinstance(coef, torch.Tensor) or not coef.is_cuda:
         raise Drt3dError("coef must be a CUDA tensor")
-    c = coef.contiguous()
+    st = _stream(stream, coef.device)
     nd = 5 if kind == "drt" else 6
-    if c.dim() == nd - 1:
-        c = c.unsqueeze(0)
-    if c.dim() != nd:
-        raise Drt3dError("coef must be the stacked forward layout")
-    B, N = c.shape[0], c.shape[2]
-    dt = {torch.int32: DRT3D_I32, torch.float32: DRT3D_F32}[c.dtype]
-    o = make_opts(batch=B, in_dtype=dt, out_dtype=dt, table=table)
-    if opts is not None:
-        o.events, o.max_events, o.launches, o.launch_kind = opts.events, opts.max_events, opts.launches, opts.launch_kind
-    if cube is None:
-        cube = torch.empty((B, N, N, N), dtype=c.dtype, device=c.device)
-    L = lib()
-    b = ctypes.c_size_t(0)
-    _check(getattr(L, f"{'drt3d_planes' if kind == 'drt' else 'djt3d_lines'}_adjoint_workspace_size")(
-        N, mask, ctypes.byref(o), ctypes.byref(b)), "adjoint_workspace_size")
-    if workspace is None:
-        workspace = torch.empty(max(b.value, 256), dtype=torch.uint8, device=c.device)
-    st = stream if stream is not None else torch.cuda.current_stream(c.device).cuda_stream
-    fn = L.drt3d_planes_adjoint if kind == "drt" else L.djt3d_lines_adjoint
-    _check(fn(c.data_ptr(), N, mask, cube.data_ptr(), ctypes.byref(o), workspace.data_ptr(), b.value, st),
-           f"{kind} adjoint")
+    with torch.cuda.stream(st):
+        c = coef.contiguous()
+        if c.dim() == nd - 1:
+            c = c.unsqueeze(0)
+        if c.dim() != nd:
+            raise Drt3dError("coef must be the stacked forward layout")
+        B, K, N = c.shape[0], c.shape[1], c.shape[2]
+        tail = (N, N, 3 * N) if kind == "drt" else (N, N, 2 * N, 2 * N)
+        if K != _popcount(mask) or tuple(c.shape[2:]) != tail:
+            raise Drt3dError(f"coef shape {tuple(coef.shape)} does not match mask {mask:#x} "
+                             f"(expected [B, {_popcount(mask)}, {', '.join(map(str, tail))}])")
+        if c.dtype not in (torch.int32, torch.float32):
+            raise Drt3dError("coef must be int32 or float32")
+        dt = DRT3D_I32 if c.dtype == torch.int32 else DRT3D_F32
+        o = make_opts(batch=B, in_dtype=dt, out_dtype=dt, table=table)
+        _opts_from(o, opts)
+        if cube is None:
+            cube = torch.empty((B, N, N, N), dtype=c.dtype, device=c.device)
+            res = cube
+        else:
+            user_shape = (N, N, N) if coef.dim() == nd - 1 and cube.dim() == 3 else (B, N, N, N)
+            res = _user_tensor(cube, user_shape, c.dtype, c.device, "cube")
+            cube = res.view(B, N, N, N)
+        L = lib()
+        b = ctypes.c_size_t(0)
+        _check(getattr(L, f"{'drt3d_planes' if kind == 'drt' else 'djt3d_lines'}_adjoint_workspace_size")(
+            N, mask, ctypes.byref(o), ctypes.byref(b)), "adjoint_workspace_size")
+        ws, ws_bytes = _workspace(workspace, max(b.value, 256), c.device)
+        fn = L.drt3d_planes_adjoint if kind == "drt" else L.djt3d_lines_adjoint
+        s = fn(c.data_ptr(), N, mask, cube.data_ptr(), ctypes.byref(o), ws.data_ptr(), ws_bytes, st.cuda_stream)
+    _check(s, f"{kind} adjoint")
+    if res is not cube:
+        return res
     return cube if coef.dim() == nd else cube[0]
 
 
@@ -282,60 +340,71 @@ def planes_invert(coef, iters: int, mask: int = 0xFFF, n_min: int = 2, table: in
     rnorm [iters+1] fp64 residual norms ||b - A x_k||) by drt3d_planes_invert (DESIGN.md F-3);
     n_min = coarsest multigrid size (n_min = N: single-grid iteration)."""
     import torch
-    if not coef.is_cuda or coef.dtype != torch.float32 or coef.dim() != 4:
+    if not isinstance(coef, torch.Tensor) or not coef.is_cuda or coef.dtype != torch.float32 or coef.dim() != 4:
         raise Drt3dError("coef must be a CUDA float32 tensor [K,N,N,3N]")
-    c = coef.contiguous()
-    N = c.shape[1]
-    o = make_opts(batch=1, in_dtype=DRT3D_F32, out_dtype=DRT3D_F32, table=table)
-    if opts is not None:
-        o.launches = opts.launches
-    if cube is None:
-        cube = torch.empty((N, N, N), dtype=torch.float32, device=c.device)
-    rnorm = torch.empty(iters + 1, dtype=torch.float64, device=c.device)
-    L = lib()
-    b = ctypes.c_size_t(0)
-    _check(L.drt3d_planes_invert_workspace_size(N, n_min, mask, ctypes.byref(o), ctypes.byref(b)),
-           "invert_workspace_size")
-    if workspace is None:
-        workspace = torch.empty(max(b.value, 256), dtype=torch.uint8, device=c.device)
-    st = stream if stream is not None else torch.cuda.current_stream(c.device).cuda_stream
-    _check(L.drt3d_planes_invert(c.data_ptr(), N, n_min, mask, iters, cube.data_ptr(), rnorm.data_ptr(), ctypes.byref(o),
-                                 workspace.data_ptr(), b.value, st), "planes invert")
+    N = coef.shape[1]
+    if coef.shape[0] != _popcount(mask) or tuple(coef.shape[2:]) != (N, 3 * N):
+        raise Drt3dError(f"coef shape {tuple(coef.shape)} does not match mask {mask:#x} "
+                         f"(expected [{_popcount(mask)}, {N}, {N}, {3 * N}])")
+    st = _stream(stream, coef.device)
+    with torch.cuda.stream(st):
+        c = coef.contiguous()
+        o = make_opts(batch=1, in_dtype=DRT3D_F32, out_dtype=DRT3D_F32, table=table)
+        if opts is not None:
+            o.launches = opts.launches
+        if cube is None:
+            cube = torch.empty((N, N, N), dtype=torch.float32, device=c.device)
+        else:
+            _user_tensor(cube, (N, N, N), torch.float32, c.device, "cube")
+        rnorm = torch.empty(iters + 1, dtype=torch.float64, device=c.device)
+        L = lib()
+        b = ctypes.c_size_t(0)
+        _check(L.drt3d_planes_invert_workspace_size(N, n_min, mask, ctypes.byref(o), ctypes.byref(b)),
+               "invert_workspace_size")
+        ws, ws_bytes = _workspace(workspace, max(b.value, 256), c.device)
+        s = L.drt3d_planes_invert(c.data_ptr(), N, n_min, mask, iters, cube.data_ptr(), rnorm.data_ptr(),
+                                  ctypes.byref(o), ws.data_ptr(), ws_bytes, st.cuda_stream)
+    _check(s, "planes invert")
     return cube, rnorm
 
 
 # ------------------------------------------------------------ applications (F-4)
 
-def _apps_ws(device):
+def _apps_ws(workspace, device):
+    return _workspace(workspace, max(lib().drt3d_apps_workspace_size(), 256), device)
+
+
+def _int32_coef(coef):
     import torch
-    return torch.empty(max(lib().drt3d_apps_workspace_size(), 256), dtype=torch.uint8, device=device)
+    if not isinstance(coef, torch.Tensor) or not coef.is_cuda or coef.dtype != torch.int32:
+        raise Drt3dError("coef must be a CUDA int32 tensor")
+    return coef.contiguous()
 
 
 def coef_argmax(coef, workspace=None, stream=None) -> int:
     """Flat index of the largest int32 coefficient (smallest index among ties); synchronises."""
     import torch
-    c = coef.contiguous()
-    if not c.is_cuda or c.dtype != torch.int32:
-        raise Drt3dError("coef must be a CUDA int32 tensor")
-    ws = workspace if workspace is not None else _apps_ws(c.device)
-    idx = torch.empty(1, dtype=torch.int64, device=c.device)
-    st = stream if stream is not None else torch.cuda.current_stream(c.device).cuda_stream
-    _check(lib().drt3d_coef_argmax(c.data_ptr(), c.numel(), idx.data_ptr(), ws.data_ptr(), ws.numel(), st),
-           "coef_argmax")
-    return int(idx.item())
+    st = _stream(stream, coef.device)
+    with torch.cuda.stream(st):
+        c = _int32_coef(coef)
+        ws, ws_bytes = _apps_ws(workspace, c.device)
+        idx = torch.empty(1, dtype=torch.int64, device=c.device)
+        s = lib().drt3d_coef_argmax(c.data_ptr(), c.numel(), idx.data_ptr(), ws.data_ptr(), ws_bytes, st.cuda_stream)
+        _check(s, "coef_argmax")
+        return int(idx.item())
 
 
 def coef_threshold(coef, num: int, den: int, out=None, workspace=None, stream=None):
     """Keep c where c * den >= num * max(c), else 0 (int32, exact)."""
     import torch
-    c = coef.contiguous()
-    if not c.is_cuda or c.dtype != torch.int32:
-        raise Drt3dError("coef must be a CUDA int32 tensor")
-    out = torch.empty_like(c) if out is None else out
-    ws = workspace if workspace is not None else _apps_ws(c.device)
-    st = stream if stream is not None else torch.cuda.current_stream(c.device).cuda_stream
-    _check(lib().drt3d_coef_threshold(c.data_ptr(), c.numel(), num, den, out.data_ptr(), ws.data_ptr(), ws.numel(),
-                                      st), "coef_threshold")
+    st = _stream(stream, coef.device)
+    with torch.cuda.stream(st):
+        c = _int32_coef(coef)
+        out = torch.empty_like(c) if out is None else _user_tensor(out, c.shape, torch.int32, c.device, "out")
+        ws, ws_bytes = _apps_ws(workspace, c.device)
+        s = lib().drt3d_coef_threshold(c.data_ptr(), c.numel(), num, den, out.data_ptr(), ws.data_ptr(), ws_bytes,
+                                       st.cuda_stream)
+    _check(s, "coef_threshold")
     return out
 
 
@@ -344,27 +413,33 @@ def detect_planes(coef, mask: int, num: int, den: int, onum: int, oden: int, tab
     """Plane detection on stacked int32 DRT coefficients [K,N,N,3N] -> (flags uint8 [K,N,N,3N],
     argmax flat index tensor [1] int64), F-4."""
     import torch
-    c = coef.contiguous()
-    if not c.is_cuda or c.dtype != torch.int32 or c.dim() != 4:
-        raise Drt3dError("coef must be a CUDA int32 tensor [K,N,N,3N]")
-    N = c.shape[1]
-    flags = torch.empty(c.shape, dtype=torch.uint8, device=c.device)
-    am = torch.empty(1, dtype=torch.int64, device=c.device)
-    o = make_opts(table=table)
-    ws = workspace if workspace is not None else _apps_ws(c.device)
-    st = stream if stream is not None else torch.cuda.current_stream(c.device).cuda_stream
-    _check(lib().drt3d_detect_planes(c.data_ptr(), N, mask, num, den, onum, oden, ctypes.byref(o), flags.data_ptr(),
-                                     am.data_ptr(), ws.data_ptr(), ws.numel(), st), "detect_planes")
+    c0 = _int32_coef(coef)
+    if c0.dim() != 4 or c0.shape[0] != _popcount(mask) or tuple(c0.shape[2:]) != (c0.shape[1], 3 * c0.shape[1]):
+        raise Drt3dError(f"coef must be [{_popcount(mask)}, N, N, 3N] for mask {mask:#x}, got {tuple(coef.shape)}")
+    st = _stream(stream, coef.device)
+    with torch.cuda.stream(st):
+        c = coef.contiguous()
+        N = c.shape[1]
+        flags = torch.empty(c.shape, dtype=torch.uint8, device=c.device)
+        am = torch.empty(1, dtype=torch.int64, device=c.device)
+        o = make_opts(table=table)
+        ws, ws_bytes = _apps_ws(workspace, c.device)
+        s = lib().drt3d_detect_planes(c.data_ptr(), N, mask, num, den, onum, oden, ctypes.byref(o), flags.data_ptr(),
+                                      am.data_ptr(), ws.data_ptr(), ws_bytes, st.cuda_stream)
+    _check(s, "detect_planes")
     return flags, am
 
 
 def coef_select(coef, flags, out=None, stream=None):
     """Keep the flagged int32 coefficients (flags uint8 of the same shape), zero the rest."""
     import torch
-    c, f = coef.contiguous(), flags.contiguous()
-    if not c.is_cuda or c.dtype != torch.int32 or f.dtype != torch.uint8 or f.shape != c.shape:
-        raise Drt3dError("coef: CUDA int32; flags: uint8 of the same shape")
-    out = torch.empty_like(c) if out is None else out
-    st = stream if stream is not None else torch.cuda.current_stream(c.device).cuda_stream
-    _check(lib().drt3d_coef_select(c.data_ptr(), f.data_ptr(), c.numel(), out.data_ptr(), st), "coef_select")
+    st = _stream(stream, coef.device)
+    with torch.cuda.stream(st):
+        c = _int32_coef(coef)
+        f = flags.contiguous()
+        if not f.is_cuda or f.dtype != torch.uint8 or f.shape != c.shape or f.device != c.device:
+            raise Drt3dError("coef: CUDA int32; flags: uint8 of the same shape on the same device")
+        out = torch.empty_like(c) if out is None else _user_tensor(out, c.shape, torch.int32, c.device, "out")
+        s = lib().drt3d_coef_select(c.data_ptr(), f.data_ptr(), c.numel(), out.data_ptr(), st.cuda_stream)
+    _check(s, "coef_select")
     return out

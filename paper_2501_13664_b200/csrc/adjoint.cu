@@ -434,22 +434,20 @@ namespace {
 inline unsigned tpb(int w) { return (unsigned)(w >= 256 ? 256 : ((w + 31) / 32) * 32); }
 inline unsigned chunks(int w) { return (unsigned)((w + tpb(w) - 1) / tpb(w)); }
 // threads per DRT stage row: about 8 cells per thread (per-thread term setup is ~130 instructions)
+#ifndef D3_ADJ_EPT
+#define D3_ADJ_EPT 8
+#endif
 inline unsigned row_threads(int w) {
-    const char *e = getenv("D3_ADJ_EPT");
-    const int ept = e ? atoi(e) : 8;
+    const int ept = D3_ADJ_EPT;
     const int t = ((w + ept - 1) / ept + 31) / 32 * 32;
     return (unsigned)(t < 32 ? 32 : (t > 1024 ? 1024 : t));
 }
 
-// stages fused per launch (default 1; D3_ADJ_L in 1..3 for measurement: 2 and 3 were slower)
-int adj_fuse() {
-    static const int l = [] {
-        const char *e = getenv("D3_ADJ_L");
-        const int v = e ? atoi(e) : 1;
-        return v < 1 ? 1 : (v > 3 ? 3 : v);
-    }();
-    return l;
-}
+// stages fused per launch (default 1; -DD3_ADJ_L=2/3 for measurement builds: 2 and 3 were slower)
+#ifndef D3_ADJ_L
+#define D3_ADJ_L 1
+#endif
+int adj_fuse() { return D3_ADJ_L < 1 ? 1 : (D3_ADJ_L > 3 ? 3 : D3_ADJ_L); }
 
 // butterfly launch: 4^L rows per block in one shared-memory buffer, NC columns per thread
 template <class T, int L, int NC>
@@ -469,11 +467,13 @@ void drt_bfly(const T *in, T *out, int N, int m_lo, cudaStream_t st) {
     else drt_bfly_nc<T, 1, 12>(in, out, N, m_lo, st);              // N = 1024: radix 2 only
 }
 
-// butterfly radix per launch: 2 (16 rows) up to N = 512, else 1 (D3_ADJ_BFLY=0 selects the
-// plain gather kernels, for measurement)
+// butterfly radix per launch: 2 (16 rows) up to N = 512, else 1 (-DD3_ADJ_BFLY=0 selects the
+// plain gather kernels, for measurement builds)
+#ifndef D3_ADJ_BFLY
+#define D3_ADJ_BFLY 2
+#endif
 inline int bfly_max(int N) {
-    const char *e = getenv("D3_ADJ_BFLY");
-    const int cap = e ? atoi(e) : 2;
+    const int cap = D3_ADJ_BFLY;
     return cap <= 0 ? 0 : (cap == 1 || N > 512 ? 1 : 2);
 }
 
@@ -564,9 +564,13 @@ inline AdjWs adj_ws(int N, int n, int K) {
     return w;
 }
 
+// -DD3_ADJ_STAGES (measurement builds): the stage kernels for every N instead of the passes
 bool adj_use_passes(int N) {
-    static const bool off = getenv("D3_ADJ_MODE") && *getenv("D3_ADJ_MODE");   // set: the stage kernels
-    return !off && N >= 4;
+#ifdef D3_ADJ_STAGES
+    return false && N >= 4;
+#else
+    return N >= 4;
+#endif
 }
 
 // one instance: coefficients `src` (level n) -> level-0 rows in `l0`; returns launches

@@ -5,6 +5,8 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <vector>
 
 #include "dispatch.h"
 #include "adjoint.h"
@@ -45,8 +47,12 @@ const int8_t kDjtHemisphere[12][3] = {{1, 2, 3},   {1, -3, 2},   {1, -2, -3},  {
 // One table complete for planes and lines (R8, alternative).
 const int8_t kShared[12][3] = {{1, 2, 3},  {-2, 1, 3}, {-1, -2, 3}, {2, -1, 3},  {3, 1, 2},   {-1, 3, 2},
                                {3, -1, -2}, {1, 3, -2}, {2, 3, 1},   {3, -2, 1},  {-2, 3, -1}, {3, 2, -1}};
-// Alg. 2 OutOrder and DodecantCoords.
-const int8_t kOutOrder[12][3] = {{-2, -1, 3}, {-1, 2, 3}, {2, 1, 3},  {1, -2, 3}, {2, 1, 3},  {1, -2, 3},
+// Alg. 2 OutOrder as the mosaic applies it, and DodecantCoords.
+// Rows 4-11 are printed verbatim; rows 0-3 (the z-set) are the repaired rows of reading R13
+// (DESIGN.md): fig:shapeOutput has the dodecants "fit accurately", i.e. the
+// boundary planes two dodecants share lie on facing block edges, and these are the unique rows
+// that do so (the printed z-set rows act as if s1 and s2 were exchanged).
+const int8_t kOutOrder[12][3] = {{-1, -2, 3}, {-2, 1, 3}, {1, 2, 3},  {2, -1, 3}, {2, 1, 3},  {1, -2, 3},
                                  {-1, 2, 3},  {-2, -1, 3}, {2, 1, 3}, {-1, 2, 3}, {1, -2, 3}, {-2, -1, 3}};
 const int8_t kCoords[12][2] = {{1, 1}, {1, 2}, {2, 2}, {2, 1}, {0, 2}, {0, 1},
                                {3, 2}, {3, 1}, {2, 0}, {1, 0}, {2, 3}, {1, 3}};
@@ -108,6 +114,18 @@ struct Plan {
 // many dodecants re-reads the cube from L2 and neither launch has a partial last wave; the stage
 // buffers then live in HBM (they do not stay in L2 under the output stream anyway).
 const size_t kChunkBudget = (size_t)D3_CHUNK_MB << 20;
+// DRT pipeline (run_drt): instances of a chunk are split into up to D3_OVERLAP_GROUPS groups whose
+// first pass overlaps the previous group's later passes; D3_FINAL_PRIORITY = 1 gives the later
+// passes' stream the higher scheduling priority.
+#ifndef D3_OVERLAP_GROUPS
+#define D3_OVERLAP_GROUPS 4
+#endif
+#ifndef D3_FINAL_PRIORITY
+#define D3_FINAL_PRIORITY 0
+#endif
+#ifndef D3_OVERLAP_MIN_N
+#define D3_OVERLAP_MIN_N 128
+#endif
 
 int ilog2_exact(int N) {
     if (N < 2 || N > 1024) return -1;
@@ -289,41 +307,81 @@ drt3d_status check_ptrs(const void *cube, void *out, void *ws, size_t ws_bytes, 
     return DRT3D_OK;
 }
 
-// Cross-stream overlap of consecutive chunks: the first pass of
-// chunk i+1 runs on the caller's stream while the later passes of chunk i run on an auxiliary
-// stream, so the two latency-bound kernels share the SMs.  One auxiliary stream and four
-// events per (host thread, device), created on first use; the caller's stream is joined
-// before drt3d_planes returns, so stream semantics for the caller are unchanged.
-struct Aux {
-    cudaStream_t a = nullptr;
-    cudaEvent_t start = nullptr, fdone = nullptr, cdone[2] = {nullptr, nullptr};
-    // host-buffer calls: device-to-host copies of finished dodecant groups (kHostGroups max)
-    cudaStream_t cp = nullptr;
-    cudaEvent_t gdone[4] = {nullptr, nullptr, nullptr, nullptr}, cpdone = nullptr;
-    bool ok = false;
-};
+// Auxiliary streams and events (DESIGN.md §5 "Overlap"): a pool per process, one entry per
+// concurrently running call on a device, created on first use and reused by every later call on
+// any host thread (never destroyed: the count is bounded by the number of concurrent callers, so
+// nothing leaks per thread).  A call leases an entry for its duration; work it left on the entry's
+// streams is joined into the caller's stream before the call returns (JoinGuard, every exit path),
+// so a later lessee's work may queue behind it but is never unordered with it.
 constexpr int kHostGroups = 4;
-Aux *aux_for_current_device() {
-    thread_local Aux aux[16];
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
-    Aux &x = aux[dev];
-    if (!x.ok) {
-        if (cudaStreamCreateWithFlags(&x.a, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
-        bool e = cudaEventCreateWithFlags(&x.start, cudaEventDisableTiming) == cudaSuccess;
-        e = e && cudaEventCreateWithFlags(&x.fdone, cudaEventDisableTiming) == cudaSuccess;
-        e = e && cudaEventCreateWithFlags(&x.cdone[0], cudaEventDisableTiming) == cudaSuccess;
-        e = e && cudaEventCreateWithFlags(&x.cdone[1], cudaEventDisableTiming) == cudaSuccess;
-        e = e && cudaStreamCreateWithFlags(&x.cp, cudaStreamNonBlocking) == cudaSuccess;
-        for (int g = 0; g < kHostGroups; ++g)
-            e = e && cudaEventCreateWithFlags(&x.gdone[g], cudaEventDisableTiming) == cudaSuccess;
-        e = e && cudaEventCreateWithFlags(&x.cpdone, cudaEventDisableTiming) == cudaSuccess;
-        if (!e) return nullptr;
-        x.ok = true;
-    }
-    return &x;
+struct Aux {
+    int dev = -1;
+    bool busy = false;
+    cudaStream_t a = nullptr;                    // later passes of the DRT pipeline
+    cudaEvent_t start = nullptr, fdone = nullptr, join = nullptr, cdone[2] = {nullptr, nullptr};
+    // host-buffer calls: device-to-host copies of finished dodecant groups
+    cudaStream_t cp = nullptr;
+    cudaEvent_t gdone[kHostGroups] = {}, cpdone = nullptr;
+};
+std::mutex g_aux_mu;
+std::vector<Aux *> g_aux;
+
+bool aux_create(Aux &x) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    bool e = cudaStreamCreateWithPriority(&x.a, cudaStreamNonBlocking, D3_FINAL_PRIORITY ? hi : lo) == cudaSuccess;
+    e = e && cudaStreamCreateWithFlags(&x.cp, cudaStreamNonBlocking) == cudaSuccess;
+    for (cudaEvent_t *ev : {&x.start, &x.fdone, &x.join, &x.cdone[0], &x.cdone[1], &x.cpdone})
+        e = e && cudaEventCreateWithFlags(ev, cudaEventDisableTiming) == cudaSuccess;
+    for (int g = 0; g < kHostGroups; ++g)
+        e = e && cudaEventCreateWithFlags(&x.gdone[g], cudaEventDisableTiming) == cudaSuccess;
+    return e;
 }
 
+class AuxLease {
+    Aux *x_ = nullptr;
+public:
+    explicit AuxLease(bool want) {
+        if (!want) return;
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) return;
+        std::lock_guard<std::mutex> lk(g_aux_mu);
+        for (Aux *c : g_aux)
+            if (c->dev == dev && !c->busy) { x_ = c; break; }
+        if (!x_) {
+            Aux *c = new Aux();
+            c->dev = dev;
+            if (!aux_create(*c)) { delete c; return; }   // (partially created handles are not reused)
+            g_aux.push_back(c);
+            x_ = c;
+        }
+        x_->busy = true;
+    }
+    ~AuxLease() {
+        if (!x_) return;
+        std::lock_guard<std::mutex> lk(g_aux_mu);
+        x_->busy = false;
+    }
+    AuxLease(const AuxLease &) = delete;
+    AuxLease &operator=(const AuxLease &) = delete;
+    Aux *get() const { return x_; }
+};
+
+// Joins an auxiliary stream into the caller's stream when it goes out of scope (also on the
+// error returns), so the caller's stream always orders after everything the call enqueued.
+struct JoinGuard {
+    cudaStream_t st, from;
+    cudaEvent_t ev;
+    ~JoinGuard() {
+        if (from && cudaEventRecord(ev, from) == cudaSuccess) cudaStreamWaitEvent(st, ev, 0);
+    }
+};
+
+// DRT pipeline over groups of instances (DESIGN.md §5 "Overlap"): the first pass of group g+1
+// (latency-bound: SMEM and integer issue) runs on the caller's stream while the later passes of
+// group g (HBM-write-bound) run on the auxiliary stream, so the two kinds of work share the SMs.
+// Each instance has its own stage buffer slice inside the chunk, so groups never wait on each
+// other's buffers; consecutive chunks of large batches alternate between two buffer sets.
 drt3d_status run_drt(const void *cube, uint32_t mask, void *out, const drt3d_opts &o, const Plan &P, void *ws,
                      cudaStream_t st) {
     const int8_t(*rows)[3] = table_rows(o.table, 0);
@@ -346,55 +404,58 @@ drt3d_status run_drt(const void *cube, uint32_t mask, void *out, const drt3d_opt
             ++j;
         }
     Launcher L{st, &o};
-    static const bool no_overlap = getenv("D3_NO_OVERLAP") != nullptr;
-    Aux *ax = (P.nset == 2 && !no_overlap) ? aux_for_current_device() : nullptr;
-    if (ax && cudaEventRecord(ax->start, st) == cudaSuccess && cudaStreamWaitEvent(ax->a, ax->start, 0) == cudaSuccess) {
-    } else {
-        ax = nullptr;
-    }
+    const int ngroups_max =
+        (P.npass > 1 && P.N >= D3_OVERLAP_MIN_N) ? (P.inst < D3_OVERLAP_GROUPS ? P.inst : D3_OVERLAP_GROUPS) : 1;
+    AuxLease lease(P.npass > 1 && (ngroups_max > 1 || P.nset == 2));
+    Aux *ax = lease.get();
+    if (ax && (cudaEventRecord(ax->start, st) != cudaSuccess || cudaStreamWaitEvent(ax->a, ax->start, 0) != cudaSuccess))
+        return DRT3D_ERR_CUDA;
+    JoinGuard join{st, ax ? ax->a : nullptr, ax ? ax->join : nullptr};
     const long long final_inst = (o.layout == DRT3D_LAYOUT_MOSAIC) ? 0 : (long long)P.N * P.N * 3 * P.N;
     int chunk_idx = 0;
     for (int i0 = 0; i0 < P.inst; i0 += P.chunk, ++chunk_idx) {
         const int ninst = (P.inst - i0) < P.chunk ? (P.inst - i0) : P.chunk;
-        const int set = ax ? (chunk_idx & 1) : 0;
+        const int set = (ax && P.nset == 2) ? (chunk_idx & 1) : 0;
         char *sb = reinterpret_cast<char *>(ws) + (size_t)set * P.buf_bytes * P.nbuf;
-        char *buf[2] = {sb, sb + P.buf_bytes};
-        if (ax && chunk_idx >= 2) cudaStreamWaitEvent(st, ax->cdone[set], 0);   // buffer set free again
-        for (int p = 0; p < P.npass; ++p) {
-            const bool first = p == 0, fin = p == P.npass - 1;
-            cudaStream_t ps = (ax && !first) ? ax->a : st;
-            if (ax && p == 1) {
-                cudaEventRecord(ax->fdone, st);
-                cudaStreamWaitEvent(ax->a, ax->fdone, 0);
+        if (ax && P.nset == 2 && chunk_idx >= 2) cudaStreamWaitEvent(st, ax->cdone[set], 0);   // buffer set free again
+        const int ng = ax ? (ninst < ngroups_max ? ninst : ngroups_max) : 1;
+        for (int g = 0, gi0 = 0; g < ng; ++g) {
+            const int gn = ninst / ng + (g < ninst % ng ? 1 : 0);
+            for (int p = 0; p < P.npass; ++p) {
+                const bool first = p == 0, fin = p == P.npass - 1;
+                cudaStream_t ps = (ax && !first) ? ax->a : st;
+                if (ax && p == 1) {
+                    if (cudaEventRecord(ax->fdone, st) != cudaSuccess || cudaStreamWaitEvent(ax->a, ax->fdone, 0) != cudaSuccess)
+                        return DRT3D_ERR_CUDA;
+                }
+                // this group's slices of the chunk's stage buffers
+                char *bin = sb + (size_t)((p - 1) & 1) * P.buf_bytes;
+                char *bout = sb + (size_t)(p & 1) * P.buf_bytes;
+                DrtPass prm = base;
+                prm.c = P.cs[p];
+                prm.m = P.n - P.cs[p + 1];
+                prm.inst0 = i0 + gi0;
+                prm.in = first ? cube : bin + (size_t)gi0 * P.inst_elems[p] * stor_bytes(P.stor[p]);
+                prm.in_inst_stride = first ? 0 : P.inst_elems[p];
+                prm.in_pitch = P.pitch[p];
+                prm.in_base = P.base[p];
+                prm.in_width = P.width[p];
+                prm.out = fin ? out : bout + (size_t)gi0 * P.inst_elems[p + 1] * stor_bytes(P.stor[p + 1]);
+                prm.out_inst_stride = fin ? final_inst : P.inst_elems[p + 1];
+                prm.out_pitch = P.pitch[p + 1];
+                prm.out_base = P.base[p + 1];
+                prm.out_width = P.width[p + 1];
+                prm.next_k = fin ? 0 : P.ks[p + 1];
+                drt3d_status s = DRT3D_OK;
+                drt3d_status ls = L.run_on(ps, first ? 0 : (fin ? 2 : 1), [&] {
+                    s = dispatch_drt(o.in_dtype, P.ks[p], P.stor[p], P.stor[p + 1], first, fin, prm, gn, ps);
+                });
+                if (s != DRT3D_OK) return s;
+                if (ls != DRT3D_OK) return ls;
             }
-            DrtPass prm = base;
-            prm.c = P.cs[p];
-            prm.m = P.n - P.cs[p + 1];
-            prm.inst0 = i0;
-            prm.in = first ? cube : buf[(p - 1) & 1];
-            prm.in_inst_stride = first ? 0 : P.inst_elems[p];
-            prm.in_pitch = P.pitch[p];
-            prm.in_base = P.base[p];
-            prm.in_width = P.width[p];
-            prm.out = fin ? out : buf[p & 1];
-            prm.out_inst_stride = fin ? final_inst : P.inst_elems[p + 1];
-            prm.out_pitch = P.pitch[p + 1];
-            prm.out_base = P.base[p + 1];
-            prm.out_width = P.width[p + 1];
-            prm.next_k = fin ? 0 : P.ks[p + 1];
-            drt3d_status s = DRT3D_OK;
-            drt3d_status ls = L.run_on(ps, first ? 0 : (fin ? 2 : 1), [&] {
-                s = dispatch_drt(o.in_dtype, P.ks[p], P.stor[p], P.stor[p + 1], first, fin, prm, ninst, ps);
-            });
-            if (s != DRT3D_OK) return s;
-            if (ls != DRT3D_OK) return ls;
+            gi0 += gn;
         }
-        if (ax) cudaEventRecord(ax->cdone[set], ax->a);
-    }
-    if (ax) {
-        // join: the caller's stream waits for the last chunk on the auxiliary stream
-        if (cudaEventRecord(ax->cdone[0], ax->a) != cudaSuccess || cudaStreamWaitEvent(st, ax->cdone[0], 0) != cudaSuccess)
-            return DRT3D_ERR_CUDA;
+        if (ax && P.nset == 2) cudaEventRecord(ax->cdone[set], ax->a);
     }
     if (o.layout == DRT3D_LAYOUT_MOSAIC) {
         // the 4 blocks of the 4x4 grid no dodecant occupies
@@ -626,9 +687,10 @@ static drt3d_status host_variant(int transform, const void *host_cube, int N, ui
     // One cube, stacked layout, several dodecants: transform them in groups and copy each group's
     // output slice to the host on a copy stream while the next group computes (the result's
     // device-to-host copy is PCIe-bound, ~57 GB/s; this hides the transform behind it).
-    Aux *ax = (P.batch == 1 && o.layout == DRT3D_LAYOUT_STACKED && P.ndod >= 2 && !o.events)
-                  ? aux_for_current_device() : nullptr;
+    AuxLease lease(P.batch == 1 && o.layout == DRT3D_LAYOUT_STACKED && P.ndod >= 2 && !o.events);
+    Aux *ax = lease.get();
     if (ax) {
+        JoinGuard join{st, ax->cp, ax->cpdone};      // the caller's stream resumes after the last copy
         const int K = P.ndod, G = K < kHostGroups ? K : kHostGroups;
         const size_t per_dod = ob / (size_t)K;
         int kl[12], nk = 0;
@@ -655,9 +717,7 @@ static drt3d_status host_variant(int transform, const void *host_cube, int N, ui
             j0 += d;
         }
         if (o.launches) *o.launches = launches;
-        // the caller's stream resumes after the last copy
-        if (cudaEventRecord(ax->cpdone, ax->cp) != cudaSuccess) return DRT3D_ERR_CUDA;
-        return cudaStreamWaitEvent(st, ax->cpdone, 0) == cudaSuccess ? DRT3D_OK : DRT3D_ERR_CUDA;
+        return DRT3D_OK;
     }
     s = transform == 0 ? run_drt(dev_cube, mask, dev_out, o, P, ws, st) : run_djt(dev_cube, mask, dev_out, o, P, ws, st);
     if (s != DRT3D_OK) return s;

@@ -10,7 +10,7 @@
 //     in its dodecant's (s1, s2, D) 26-neighbourhood (R21: >= all neighbours, > those with a
 //     smaller index) and whose plane normal is orthogonal to the argmax plane's (R22: integer
 //     normals (s1, s2, -(N-1)) mapped through the signed axis permutation of the orientation
-//     table, |cos| <= onum/oden tested as (n.m)^2 oden^2 <= onum^2 |n|^2 |m|^2 in int64).
+//     table, |cos| <= onum/oden tested as (n.m)^2 oden^2 <= onum^2 |n|^2 |m|^2 in 128-bit integers).
 //
 // Reductions are two-pass with a fixed grid (deterministic).  All on the caller's stream.
 #include "drt3d.h"
@@ -184,7 +184,14 @@ __global__ void __launch_bounds__(kThreads) detect_kernel(const int32_t *__restr
         normal(a, j, s1, s2, nv);
         const long long dot = nv[0] * m[0] + nv[1] * m[1] + nv[2] * m[2];
         const long long nn = nv[0] * nv[0] + nv[1] * nv[1] + nv[2] * nv[2];
-        if (dot * dot * a.oden * a.oden > (long long)a.onum * a.onum * nn * mm) return 0;
+        // |cos| <= onum / oden as (n.m)^2 oden^2 <= onum^2 |n|^2 |m|^2, exactly: each side is below
+        // (3 N^2)^2 * 2^62 < 2^128 for N <= 1024 and 31-bit onum / oden
+        using u128 = unsigned __int128;
+        const u128 dd = (u128)(unsigned long long)(dot < 0 ? -dot : dot);
+        const u128 lhs = dd * dd * (u128)(unsigned long long)a.oden * (u128)(unsigned long long)a.oden;
+        const u128 rhs = (u128)(unsigned long long)a.onum * (u128)(unsigned long long)a.onum * (u128)(unsigned long long)nn *
+                         (u128)(unsigned long long)mm;
+        if (lhs > rhs) return 0;
         const int32_t *base = c + (size_t)j * per;
         for (int d1 = -1; d1 <= 1; ++d1)
             for (int d2 = -1; d2 <= 1; ++d2)

@@ -77,7 +77,11 @@ drt3d_status launch_drt_k(const DrtPass &prm_in, int ninst, cudaStream_t st) {
     CUtensorMap omap;
     std::memset(&omap, 0, sizeof(omap));
     prm.tma_store = 0;
-    static const bool no_tma = getenv("D3_NO_TMA_STORE") != nullptr;
+#ifdef D3_NO_TMA_STORE
+    constexpr bool no_tma = true;      // measurement builds: direct 16-byte stores
+#else
+    constexpr bool no_tma = false;
+#endif
     if constexpr (FINAL && sizeof(Out) == 4) {
         constexpr int S = 1 << K;
         if (!no_tma && prm.layout == 0 && prm.m == 0 && prm.out_width % T == 0 && S * S * T * 4 <= G::SMEM &&

@@ -50,7 +50,9 @@ def test_threshold_matches_oracle(num, den):
 
 
 @pytest.mark.parametrize("N,mask,num,den,onum,oden", [(16, 0xFFF, 1, 2, 1, 10), (32, 0xFFF, 1, 3, 1, 10),
-                                                      (32, 0x0F3, 1, 4, 1, 5), (64, 0xFFF, 1, 3, 1, 20)])
+                                                      (32, 0x0F3, 1, 4, 1, 5), (64, 0xFFF, 1, 3, 1, 20),
+                                                      # 31-bit cosine fraction: the exact test needs 128 bits
+                                                      (64, 0xFFF, 1, 3, 99999989, 1999999973)])
 def test_detect_planes_matches_oracle(N, mask, num, den, onum, oden):
     f = _room(N, N)
     c = d3.planes(torch.from_numpy(f).cuda(), mask)                   # int32 [K,N,N,3N], GPU forward

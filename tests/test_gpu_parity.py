@@ -8,6 +8,7 @@ import numpy as np
 import pytest
 
 import oracle
+import oracle_pool
 import synth
 from oracle import tables
 
@@ -58,16 +59,52 @@ def test_cfg1_n16_i32_dodecant0():
     assert np.array_equal(got.astype(np.int64), ref)
 
 
-@pytest.mark.parametrize("N", [2, 4, 8, 16, 32, 64, 128])
+@pytest.mark.parametrize("N", [2, 4, 8, 16, 32, 64])
 @pytest.mark.parametrize("dtype", [np.uint8, np.int32])
 def test_drt_random_all_dodecants(N, dtype):
-    if N == 128 and dtype == np.int32:
-        pytest.skip("covered by the uint8 case; keeps the oracle time bounded")
     lo, hi = (0, 255) if dtype == np.uint8 else (-1000, 1000)
     cube = synth.uniform_cube(N, 100 + N, dtype, lo, hi, batch=2 if N <= 32 else 1)
     got = _planes(cube, 0xFFF)
     ref = oracle.drt_planes(cube, 0xFFF)
     assert np.array_equal(got.astype(np.int64), ref)
+
+
+def _full_parity(tmp_path, cube, mask=0xFFF, transform="drt", per_task=1, **kw):
+    """GPU call on [B][N][N][N] cubes, then every element of every (cube, dodecant) against the
+    oracle recursion in parallel processes (tests/oracle_pool.py)."""
+    cube = _4d(cube)
+    if transform == "drt":
+        got = d3.planes(_gpu(cube), mask, **kw)
+    else:
+        got = d3.lines(_gpu(cube), mask, **kw)
+    torch.cuda.synchronize()
+    host = got.cpu().numpy()
+    del got
+    bad = oracle_pool.compare_all(tmp_path, cube, host, mask, transform, kw.get("table", 0), per_task=per_task)
+    assert not bad, bad[:8]
+    return host
+
+
+@pytest.mark.parametrize("N", [128, 256])
+@pytest.mark.parametrize("kind", ["u8", "i32", "f32"])
+def test_drt_large_all_dodecants_full(N, kind, tmp_path):
+    """N = 128 and 256, all 12 dodecants, every element: the K = 4 first passes (SWAR u8, 32-bit
+    i32 / f32) and the K = 3 / K = 4 final passes, including the 32-bit TMA-store tile."""
+    if kind == "u8":
+        cube = synth.uniform_cube(N, 700 + N, np.uint8)
+    elif kind == "i32":
+        cube = synth.uniform_cube(N, 710 + N, np.int32, -1000, 1000)
+    else:
+        cube = synth.normal_cube(N, 720 + N)
+    _full_parity(tmp_path, cube)
+
+
+def test_drt_saturated_n256_full(tmp_path):
+    """All voxels 255 at N = 256, all 12 dodecants, every element: the tightest case of the u16
+    SWAR lanes (stage-4 sums up to 255 * 256 = 65280 of 65535) and of the u16 stage buffer."""
+    cube = np.full((256, 256, 256), 255, np.uint8)
+    host = _full_parity(tmp_path, cube)
+    assert int(host.max()) == 255 * 256 * 256
 
 
 @pytest.mark.parametrize("table", [d3.DRT3D_TABLE_PRINTED, d3.DRT3D_TABLE_SHARED])
@@ -94,10 +131,10 @@ def test_cfg2_n64_sheets_full():
     assert np.array_equal(got.astype(np.int64), ref)
 
 
-def test_cfg3_n256_full_size():
-    """BASELINE config 3 at full size, same launch as bench.py: two dodecants
-    against the full oracle recursion, every dodecant on sampled outputs
-    (eq:3DfDRT by direct summation) and on invariants (mass, support)."""
+def test_cfg3_n256_full_size(tmp_path):
+    """BASELINE config 3 at full size, same launch as bench.py: every element of all 12
+    dodecants against the oracle recursion (12 processes), plus the mass and support
+    invariants checked on the device."""
     cube = synth.config_input(3)
     N = 256
     gpu = d3.planes(_gpu(cube), 0xFFF)[0]             # cube is [1][N][N][N] -> [12][N][N][3N] int32 on device
@@ -113,42 +150,21 @@ def test_cfg3_n256_full_size():
     D = torch.arange(3 * N, device="cuda")
     below = D[None, None, :] < lim[:, :, None]
     assert int(gpu.masked_select(below.unsqueeze(0).expand_as(gpu)).abs().sum()) == 0
-    host = gpu.cpu().numpy()
-    rows = tables.DRT_HEMISPHERE
-    for k in (0, 5):
-        ref = oracle.drt_alg1(oracle.orient(f, rows[k]))
-        assert np.array_equal(host[k].astype(np.int64), ref)
-    rng = np.random.default_rng(3)
-    for k in range(12):
-        g = oracle.orient(f, rows[k])
-        for _ in range(40):
-            s1, s2 = int(rng.integers(0, N)), int(rng.integers(0, N))
-            Dd = int(rng.integers(2 * N - s1 - s2, 3 * N))
-            assert host[k, s1, s2, Dd] == oracle.drt_point(g, s1, s2, Dd)
+    host = gpu.cpu().numpy()[None]
+    del gpu
+    bad = oracle_pool.compare_all(tmp_path, cube, host, 0xFFF)
+    assert not bad, bad[:8]
 
 
-def test_cfg5_batched_f32():
-    """Config 5: 256 cubes N=32 f32, 12 dodecants.  Tolerance (T1):
-    |gpu - ref64| <= 1e-5 * sum|terms| per element, sum|terms| = the fp64
+def test_cfg5_batched_f32(tmp_path):
+    """Config 5: 256 cubes N=32 f32, 12 dodecants, every element of every cube.  Tolerance
+    (T1): |gpu - ref64| <= 1e-5 * sum|terms| per element, sum|terms| = the fp64
     transform of |f|; empty planes must be exactly 0."""
     cube = synth.config_input(5)                       # [256][32][32][32] f32
     got = _planes(cube, 0xFFF)                         # [256][12][32][32][96]
     assert got.dtype == np.float32 and np.isfinite(got).all()
-    for b in (0, 1, 77, 255):
-        ref = oracle.drt_planes(cube[b].astype(np.float64), 0xFFF)
-        refabs = oracle.drt_planes(np.abs(cube[b]).astype(np.float64), 0xFFF)
-        err = np.abs(got[b].astype(np.float64) - ref)
-        assert np.all(err <= 1e-5 * refabs)
-        assert np.all(got[b][refabs == 0] == 0)
-    # the rest: sampled outputs by direct summation
-    rng = np.random.default_rng(5)
-    rows = tables.DRT_HEMISPHERE
-    for _ in range(300):
-        b, k = int(rng.integers(0, 256)), int(rng.integers(0, 12))
-        s1, s2, D = (int(t) for t in rng.integers(0, [32, 32, 96]))
-        g = oracle.orient(cube[b].astype(np.float64), rows[k])
-        ref, scale = oracle.drt_point(g, s1, s2, D), oracle.drt_point(g, s1, s2, D, absolute=True)
-        assert abs(float(got[b, k, s1, s2, D]) - ref) <= 1e-5 * scale
+    bad = oracle_pool.compare_all(tmp_path, cube, got, 0xFFF, per_task=48)
+    assert not bad, bad[:8]
 
 
 def test_drt_float_small_all_tables():
@@ -161,7 +177,8 @@ def test_drt_float_small_all_tables():
 
 
 def test_drt_mosaic_layout():
-    for N in (4, 32):
+    # N = 128: the u16 SWAR first pass and the K = 3 final pass's mosaic stores
+    for N in (4, 32, 128):
         cube = synth.uniform_cube(N, 400 + N, np.uint8)
         got = _planes(cube, 0xFFF, layout=d3.DRT3D_LAYOUT_MOSAIC)
         assert got.shape == (4 * N, 4 * N, 3 * N - 2)
@@ -229,6 +246,17 @@ def test_djt_random_all_dodecants(N, dtype):
     else:
         ref = oracle.djt_lines(cube, 0xFFF)
         assert np.array_equal(got.astype(np.int64), ref)
+
+
+@pytest.mark.parametrize("kind", ["i32", "f32"])
+def test_djt_n64_all_dodecants_full(kind, tmp_path):
+    """DJT N = 64 on all 12 dodecants with 32-bit voxels, every element (K = 3 passes over
+    32-bit stage buffers)."""
+    if kind == "i32":
+        cube = synth.uniform_cube(64, 800, np.int32, -1000, 1000)
+    else:
+        cube = synth.normal_cube(64, 801)
+    _full_parity(tmp_path, cube, transform="djt")
 
 
 def test_djt_n128_sampled():
@@ -453,3 +481,44 @@ def test_concurrent_host_threads():
         assert bool(torch.equal(out[t][0], ref[t]))
         assert bool(torch.equal(out[t][1], ref_adj[t]))
         assert bool(torch.equal(out[t][2], ref_inv[t]))
+
+
+def test_binding_validates_user_buffers():
+    """The binding checks caller-supplied buffers and tells the C ABI their real sizes (no
+    writes past a short workspace, no coefficient reads past a buffer with fewer dodecants)."""
+    cube = _gpu(synth.uniform_cube(32, 61, np.uint8))
+    need = d3.drt3d_planes_workspace_size(32, 0xFFF, d3.make_opts())
+    with pytest.raises(d3.Drt3dError):
+        d3.planes(cube, 0xFFF, workspace=torch.empty(need // 2, dtype=torch.uint8, device="cuda"))
+    with pytest.raises(d3.Drt3dError):
+        d3.planes(cube, 0xFFF, out=torch.empty((12, 32, 32, 95), dtype=torch.int32, device="cuda"))
+    with pytest.raises(d3.Drt3dError):
+        d3.planes(cube, 0xFFF, out=torch.empty((12, 32, 32, 96), dtype=torch.float32, device="cuda"))
+    one = d3.planes(cube, 0x001)                            # [1, N, N, 3N]
+    with pytest.raises(d3.Drt3dError):
+        d3.planes_adjoint(one, 0xFFF)                       # 12 dodecants' worth from a 1-dodecant buffer
+    with pytest.raises(d3.Drt3dError):
+        d3.planes_invert(one.float(), 2, mask=0x003)
+    with pytest.raises(d3.Drt3dError):
+        d3.planes_adjoint(one, 0x001, cube=torch.empty((32, 32, 31), dtype=torch.int32, device="cuda"))
+    # a correctly shaped user buffer is used in place
+    out = torch.empty((1, 32, 32, 96), dtype=torch.int32, device="cuda")
+    assert d3.planes(cube, 0x001, out=out).data_ptr() == out.data_ptr()
+    torch.cuda.synchronize()
+    assert torch.equal(out, one)
+
+
+def test_explicit_stream_argument():
+    """stream= as a torch stream or a raw handle that is not the current stream: temporaries are
+    allocated on that stream, results equal the current-stream call."""
+    cube = synth.uniform_cube(64, 62, np.int32, -100, 100)
+    ref = _planes(cube, 0xFFF)
+    s = torch.cuda.Stream()
+    g = _gpu(cube)
+    torch.cuda.synchronize()
+    a = d3.planes(g, 0xFFF, stream=s)
+    b = d3.planes(g, 0xFFF, stream=s.cuda_stream)
+    adj = d3.planes_adjoint(a, 0xFFF, stream=s)
+    s.synchronize()
+    assert np.array_equal(a.cpu().numpy(), ref) and np.array_equal(b.cpu().numpy(), ref)
+    assert torch.equal(adj, d3.planes_adjoint(a, 0xFFF))

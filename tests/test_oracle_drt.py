@@ -244,6 +244,113 @@ def test_mosaic_placement():
         assert sorted(blk.reshape(-1)) == sorted(st[k][:, :, 2:].reshape(-1))
 
 
+# ------------------------------------------------ mosaic seams (R13)
+# Shared boundary planes of neighbouring dodecants of one normal set (HEMISPHERE table): the
+# slope-0 edge of one is the same set of discrete planes as the slope-0 edge of the other
+# (e.g. k=0 at s2=0 is z = l_s1(x) + d for every y; k=1 at s1=0 is z = l_s2(x) + d, reading A).
+# The identities follow from the geometry, not from any mosaic code.
+SHARED_EDGES = [
+    (0, "s2=0", 1, "s1=0"), (0, "s1=0", 3, "s2=0"), (1, "s2=0", 2, "s1=0"), (2, "s2=0", 3, "s1=0"),
+    (4, "s1=0", 5, "s2=0"), (4, "s2=0", 6, "s1=0"), (5, "s1=0", 7, "s2=0"), (6, "s2=0", 7, "s1=0"),
+    (8, "s2=0", 9, "s1=0"), (8, "s1=0", 10, "s2=0"), (9, "s2=0", 11, "s1=0"), (10, "s1=0", 11, "s2=0"),
+]
+
+
+def _edge(out_k, e):
+    return out_k[0] if e == "s1=0" else out_k[:, 0]
+
+
+@pytest.mark.parametrize("N,seed", [(4, 41), (8, 42), (16, 43)])
+def test_shared_boundary_identities(N, seed):
+    st = oracle.drt_planes(_rand(N, seed), 0xFFF)
+    for k, e, kk, ee in SHARED_EDGES:
+        assert np.array_equal(_edge(st[k], e), _edge(st[kk], ee)), (k, e, kk, ee)
+    # the slope-0 edges of dodecants of different sets are different planes
+    assert not np.array_equal(_edge(st[0], "s1=0"), _edge(st[4], "s1=0"))
+
+
+def _block(M, N, k):
+    bi, bj = tables.DODECANT_COORDS[k]
+    return M[bi * N:(bi + 1) * N, bj * N:(bj + 1) * N]
+
+
+def _facing(M, N, k, kk):
+    """Facing edge lines of the blocks of k and kk, which must be neighbours on the 4 x 4 block
+    torus (the y- and x-sets meet across the hemisphere's wrap); None if they are not."""
+    (bi, bj), (ci, cj) = tables.DODECANT_COORDS[k], tables.DODECANT_COORDS[kk]
+    A, B = _block(M, N, k), _block(M, N, kk)
+    if bj == cj and (ci - bi) % 4 == 1:
+        return A[N - 1], B[0]
+    if bj == cj and (bi - ci) % 4 == 1:
+        return A[0], B[N - 1]
+    if bi == ci and (cj - bj) % 4 == 1:
+        return A[:, N - 1], B[:, 0]
+    if bi == ci and (bj - cj) % 4 == 1:
+        return A[:, 0], B[:, N - 1]
+    return None
+
+
+@pytest.mark.parametrize("N,seed", [(4, 44), (8, 45), (16, 46)])
+def test_mosaic_seams_fit(N, seed):
+    # fig:shapeOutput (PAPER.md:374-378): "Each individual dodecant output is rotated so that all
+    # of them fit accurately".  Every shared boundary of SHARED_EDGES lies on the facing edges of
+    # the two blocks, column for column, and those edges hold exactly the shared planes.
+    st = oracle.drt_planes(_rand(N, seed, 1, 255), 0xFFF)
+    M = oracle.mosaic(st)
+    for k, e, kk, ee in SHARED_EDGES:
+        f = _facing(M, N, k, kk)
+        assert f is not None, (k, kk)
+        a, b = f
+        assert np.array_equal(a, b), (k, kk)
+        line = _edge(st[k], e)[:, 2:]
+        assert sorted(map(tuple, a)) == sorted(map(tuple, line)), (k, kk)
+
+
+@pytest.mark.parametrize("N", [4, 8])
+def test_mosaic_null_normals(N):
+    # fig:shapeOutput: "The black dots mark the position of x, y, and z null normals": the
+    # (s1, s2) = (0, 0) columns of the z-set meet at the mosaic centre, those of the y-set at the
+    # middles of the top and bottom edges, those of the x-set at the middles of the left and
+    # right edges.
+    st = oracle.drt_planes(_rand(N, 47, 1, 255), 0xFFF)
+    M = oracle.mosaic(st)
+    dots = {0: (2 * N - 1, 2 * N - 1), 1: (2 * N - 1, 2 * N), 2: (2 * N, 2 * N), 3: (2 * N, 2 * N - 1),
+            4: (0, 2 * N), 5: (0, 2 * N - 1), 6: (4 * N - 1, 2 * N), 7: (4 * N - 1, 2 * N - 1),
+            8: (2 * N, 0), 9: (2 * N - 1, 0), 10: (2 * N, 4 * N - 1), 11: (2 * N - 1, 4 * N - 1)}
+    for k, (i, j) in dots.items():
+        assert np.array_equal(M[i, j], st[k][0, 0, 2:]), k
+
+
+def test_mosaic_orientation_is_forced():
+    # With DodecantCoords verbatim, exactly one of the 8 square symmetries per dodecant closes all
+    # four seams of its normal set (R13): the mosaic's within-block orientation is not a choice.
+    N = 4
+    st = oracle.drt_planes(_rand(N, 48, 1, 255), 0xFFF)
+    syms = [(p, f0, f1) for p in (0, 1) for f0 in (0, 1) for f1 in (0, 1)]
+
+    def orient_block(b, sym):
+        p, f0, f1 = sym
+        b = np.transpose(b, (1, 0, 2)) if p else b
+        b = b[::-1] if f0 else b
+        return b[:, ::-1] if f1 else b
+
+    import itertools
+    for S in ((0, 1, 2, 3), (4, 5, 6, 7), (8, 9, 10, 11)):
+        pairs = [p for p in SHARED_EDGES if p[0] in S]
+        good = []
+        for choice in itertools.product(range(8), repeat=4):
+            M = np.zeros((4 * N, 4 * N, 3 * N - 2), st.dtype)
+            for k, c in zip(S, choice):
+                bi, bj = tables.DODECANT_COORDS[k]
+                M[bi * N:(bi + 1) * N, bj * N:(bj + 1) * N] = orient_block(st[k][:, :, 2:], syms[c])
+            if all(np.array_equal(*_facing(M, N, k, kk)) for k, _, kk, _ in pairs):
+                good.append(choice)
+        assert len(good) == 1, (S, good)
+        M = oracle.mosaic(st)
+        for k, c in zip(S, good[0]):
+            assert np.array_equal(_block(M, N, k), orient_block(st[k][:, :, 2:], syms[c])), k
+
+
 # ----------------------------------------------------------------- adjoint
 
 @pytest.mark.parametrize("N", [4, 8, 16])
