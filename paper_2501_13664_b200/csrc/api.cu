@@ -105,6 +105,7 @@ struct Plan {
     int nset;               // 2: consecutive chunks use alternate buffer sets (cross-stream overlap)
     size_t ws_bytes;
     int nlaunch;
+    int small;              // 1: the on-chip N = 32 kernel (k_small.cu), one launch, no workspace
 };
 
 #ifndef D3_CHUNK_MB
@@ -224,6 +225,17 @@ drt3d_status make_plan(int transform, int N, uint32_t mask, const drt3d_opts &o,
         }
     }
     P.base[0] = transform == 0 ? 2 * N : N;
+#ifndef D3_NO_SMALL32
+    if (transform == 0 && N == 32 && o.layout == DRT3D_LAYOUT_STACKED) {
+        // all stages on chip in one cluster per instance: no stage buffers
+        P.small = 1;
+        P.chunk = P.inst;
+        P.nset = 1;
+        P.ws_bytes = 0;
+        P.nlaunch = 1;
+        return DRT3D_OK;
+    }
+#endif
     P.width[0] = N;
     size_t per_inst = 0;
     for (int p = 1; p < P.npass; ++p) {
@@ -404,6 +416,16 @@ drt3d_status run_drt(const void *cube, uint32_t mask, void *out, const drt3d_opt
             ++j;
         }
     Launcher L{st, &o};
+    if (P.small) {
+        base.inst0 = 0;
+        base.in = cube;
+        base.out = out;
+        drt3d_status s = DRT3D_OK;
+        drt3d_status ls = L.run(2, [&] { s = dispatch_drt_small32(o.in_dtype, base, P.inst, st); });
+        if (s != DRT3D_OK) return s;
+        if (o.launches) *o.launches = L.count;
+        return ls;
+    }
     const int ngroups_max =
         (P.npass > 1 && P.N >= D3_OVERLAP_MIN_N) ? (P.inst < D3_OVERLAP_GROUPS ? P.inst : D3_OVERLAP_GROUPS) : 1;
     AuxLease lease(P.npass > 1 && (ngroups_max > 1 || P.nset == 2));
