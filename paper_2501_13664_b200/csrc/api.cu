@@ -119,7 +119,7 @@ const size_t kChunkBudget = (size_t)D3_CHUNK_MB << 20;
 // first pass overlaps the previous group's later passes; D3_FINAL_PRIORITY = 1 gives the later
 // passes' stream the higher scheduling priority.
 #ifndef D3_OVERLAP_GROUPS
-#define D3_OVERLAP_GROUPS 4
+#define D3_OVERLAP_GROUPS 1
 #endif
 #ifndef D3_FINAL_PRIORITY
 #define D3_FINAL_PRIORITY 0
@@ -225,9 +225,11 @@ drt3d_status make_plan(int transform, int N, uint32_t mask, const drt3d_opts &o,
         }
     }
     P.base[0] = transform == 0 ? 2 * N : N;
-#ifndef D3_NO_SMALL32
+#ifdef D3_SMALL32
+    // measurement builds (-DD3_SMALL32): every stage on chip in one 8-CTA cluster per instance
+    // (k_small.cu), no stage buffers.  Measured slower than the two passes for fp32 and int32
+    // (cfg5: 1.06 vs 0.83 ms, DESIGN.md §5 "On-chip N = 32"), faster for u8 (1.00 vs 1.24 ms).
     if (transform == 0 && N == 32 && o.layout == DRT3D_LAYOUT_STACKED) {
-        // all stages on chip in one cluster per instance: no stage buffers
         P.small = 1;
         P.chunk = P.inst;
         P.nset = 1;

@@ -15,10 +15,12 @@
 // Phase 1 is an all-to-all into phase 2 (every column block feeds every slope group), so one
 // instance is a cluster of 8 CTAs exchanging through distributed shared memory: CTA q computes
 // column blocks 2q, 2q+1 and owns the slope groups sigma1 = q (8 groups x 16 rows).  Each f3 row
-// is written straight into its owner's shared memory, pre-shifted by sigma1 V1 + sigma2 V2 (the
-// runtime part of the phase-2 offsets), so phase 2's sums use compile-time register offsets
-// only.  Both phases use drt_accumulate (separable x-step then y-step, register-blocked runs of
-// R = 8 outputs) on 32-bit lanes: integer sums mod 2^32, or fp32.
+// is written straight into its owner's shared memory as aligned 16-byte chunks (realigned with
+// one warp shuffle), at a residual shift that makes the runtime part of the phase-2 offsets,
+// sigma1 V1 + sigma2 V2, a whole number of chunks: phase 2 adds a per-row chunk offset to its
+// shared-memory addresses and keeps compile-time register offsets for the rest.  Both phases are
+// separable direct sums (x-step then y-step) over register-blocked runs of R outputs on 32-bit
+// lanes: integer sums mod 2^32, or fp32.
 #include <cooperative_groups.h>
 
 #include "dispatch.h"
@@ -28,52 +30,81 @@ namespace cg = cooperative_groups;
 namespace d3 {
 namespace small32 {
 
-constexpr int N = 32, CL = 8, R = 8, THREADS = 128;
-// phase 1: a column block = 64 slots (w1, w2); slot element e holds z' = e - 16
-// (the x-step output X covers e in [0, 56), f3 e in [0, 48): z in [-16, 32) -- f3 vanishes
-// below z = -14, the support start of stage 3).
-constexpr int E0 = 16;
-constexpr int NB = 16 / CL;                   // column blocks per CTA
-constexpr int NRX1 = 7, NRY1 = 6;
+constexpr int N = 32, CL = 8, THREADS = 256;
+// ---- phase 1: one column block at a time (two per CTA), 64 slots (w1, w2) of SP1 bytes; slot
+// element e holds z' = e - 16.  The x-step output X covers e in [0, 56) (14 runs of R1 = 4), f3
+// e in [0, 48) (12 runs): z in [-16, 32) -- f3 vanishes below z = -14, the support start of
+// stage 3.
+constexpr int R1 = 4, NB = 16 / CL, NRX1 = 14, NRY1 = 12;
 constexpr int SP1 = 64 * 4 + 16;              // 64 staged words (X needs 56); +16 rotates banks
-constexpr int SM1 = NB * 64 * SP1;
-// phase 2: 8 groups (sigma2) x 16 rows (V1, V2) of stored f3.  Stored element p of row
-// (sigma, V) holds f3(sigma | V) at z = zb + p + sigma1 V1 + sigma2 V2, zb = -(4 sigma1 +
-// 4 sigma2 + 8): the group's output window z in [zb, 32) has Wout = 40 + 4 (sigma1 + sigma2)
-// <= 96 elements (D = p + 56 - 4 (sigma1 + sigma2), a multiple of 4: 16-byte stores).
-constexpr int NRX2 = 13, NRY2 = 12;           // runs for the widest group (Wout = 96, +3 halo)
-constexpr int SP2 = 112 * 4 + 16;             // x-step reads < 108 elements, X2 is 104 words
-constexpr int GROUP_BYTES = 16 * SP2;
-constexpr int SM2 = 8 * GROUP_BYTES;
-constexpr int SMEM = SM1 + SM2;
+constexpr int SMA = NB * 64 * SP1;            // area A: phase-1 staging (both blocks), later phase-2 X2 rows
+// ---- phase 2 input, area B: 8 groups (sigma2) x 16 rows (V = 4 V1 + V2) of 14 chunks.  Row
+// (sigma, V) stores f3(sigma | V)[z] at element k = z + 16 + shift, shift = A - u in [0, 4),
+// u = 16 + zb + sigma1 V1 + sigma2 V2, A = 4 ceil(u / 4), zb = -(4 sigma1 + 4 sigma2 + 8): the
+// reader of output element p (z = zb + p) then needs element p + l + A, i.e. chunk offset A / 4.
+// Chunks outside [0, 14) read as zero (one zero chunk).
+constexpr int NCHB = 14, RB = NCHB * 16 + 16;
+constexpr int SMB = 8 * 16 * RB;
+// ---- phase 2: group sigma = (q, g) has the output window z in [zb, 32), Wout = 40 + 4 (q + g)
+// <= 96 elements, D = p + 56 - 4 (q + g) (a multiple of 4: 16-byte stores); X2 rows (rho1, V2)
+// in area A, two groups at a time.
+constexpr int R2 = 8, NRX2 = 13, NRY2 = 12;   // runs for the widest group (Wout = 96, +3 halo)
+constexpr int SPX = 104 * 4 + 16;
+constexpr int GP = 4;                         // phase-2 groups at a time
+static_assert(GP * 16 * SPX <= SMA, "X2 rows of GP groups fit area A");
+constexpr int SMEM = SMA + SMB + 16;
 
-__device__ __forceinline__ int elem_off(int p) { return 16 * xswz(p >> 2) + 4 * (p & 3); }
+// acc[r][j] += sum_a row_a[c0 chunks + co[a] chunks + j + l^K_r(a)] over the S rows `row[a]` of
+// area B (NCHB chunks each, XOR-swizzled); chunks outside [0, NCHB) read the zero chunk.
+template <int K, int R, class Acc>
+__device__ __forceinline__ void acc_rows_b(const unsigned char *const (&row)[1 << K], const int (&co)[1 << K], int c0,
+                                           const unsigned char *zero, uint32_t one, Acc (&acc)[1 << K][R]) {
+    constexpr int S = 1 << K;
+    auto load = [&](int a, int ne, uint32_t *buf) {
+#pragma unroll
+        for (int i = 0; i < (ne + 3) / 4; ++i) {
+            const int c = co[a] + c0 + i;
+            const unsigned char *src = (unsigned)c < (unsigned)NCHB ? row[a] + 16 * xswz(c) : zero;
+            const uint4 v = *reinterpret_cast<const uint4 *>(src);
+            buf[4 * i + 0] = v.x;
+            if (4 * i + 1 < ne) buf[4 * i + 1] = v.y;
+            if (4 * i + 2 < ne) buf[4 * i + 2] = v.z;
+            if (4 * i + 3 < ne) buf[4 * i + 3] = v.w;
+        }
+    };
+    static_for<0, S / 2>([&](auto p_) {
+        constexpr int a0 = 2 * decltype(p_)::value, a1 = a0 + 1;
+        uint32_t b0[R + a0], b1[R + a1];
+        load(a0, R + a0, b0);
+        load(a1, R + a1, b1);
+        static_for<0, S>([&](auto r_) {
+            constexpr int r = decltype(r_)::value;
+            constexpr int o0 = lk(K, r, a0), o1 = lk(K, r, a1);
+#pragma unroll
+            for (int j = 0; j < R; ++j) acc[r][j] = add2<Acc>(acc[r][j], b0[j + o0], b1[j + o1], one, (r & 3) == 0);
+        });
+    });
+}
 
 template <class In, class Acc>
-__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(THREADS)
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(THREADS, 3)
 drt_small32_kernel(const DrtPass p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    unsigned char *sm1 = smem_raw, *sm2 = smem_raw + SM1;
+    unsigned char *smA = smem_raw, *smB = smem_raw + SMA, *zero = smem_raw + SMA + SMB;
     cg::cluster_group cluster = cg::this_cluster();
     const int q = (int)cluster.block_rank();                 // owns sigma1 = q
     const int li = blockIdx.x / CL;                          // instance of this launch
     const int inst = p.inst0 + li;
     const int tid = threadIdx.x;
+    const Orient o = p.ori[inst % p.ndod];
+    const In *cube = reinterpret_cast<const In *>(p.in) + (long long)(inst / p.ndod) * N * N * N;
 
-    // ---- zero this CTA's phase-2 rows (f3 lands on its support only), then a cluster barrier:
-    // every CTA of the cluster has started and zeroed before any remote write
-    for (int i = tid; i < SM2 / 16; i += THREADS) reinterpret_cast<uint4 *>(sm2)[i] = make_uint4(0u, 0u, 0u, 0u);
-
-    // ---- phase 1 staging: slots (blk, w1, w2), stage-0 rows of column blocks 2q, 2q+1
-    // (orientation as an index remap, reading A: element (x', y', z') at off0 + x' sx + y' sy + z' sz)
-    {
-        const Orient o = p.ori[inst % p.ndod];
-        const In *cube = reinterpret_cast<const In *>(p.in) + (long long)(inst / p.ndod) * N * N * N;
-        // item = (slot, chunk c of 16): chunks 4..11 hold z' = 4 (c - 4) .. + 3, the rest zeros
+    // stage-0 rows of column block b into area A: slot (w1, w2), chunk c holds z' = 4 (c - 4) .. + 3
+    // (zeros outside the cube); orientation as an index remap (reading A)
+    auto stage = [&]() {
         for (int it = tid; it < NB * 64 * 16; it += THREADS) {
-            const int slot = it >> 4, c = it & 15;
-            const int blk = slot >> 6, w1 = (slot >> 3) & 7, w2 = slot & 7;
-            const int b = NB * q + blk, V1 = b >> 2, V2 = b & 3;
+            const int slot = it >> 4, c = it & 15, w1 = (slot >> 3) & 7, w2 = slot & 7;
+            const int b = NB * q + (slot >> 6), V1 = b >> 2, V2 = b & 3;
             uint32_t v[4] = {0u, 0u, 0u, 0u};
             if (c >= 4 && c < 12) {
                 const int z4 = 4 * (c - 4);
@@ -97,106 +128,144 @@ drt_small32_kernel(const DrtPass p) {
                     for (int k = 0; k < 4; ++k) v[k] = Elem<In>::load_bits(cube + base + (long long)(z4 + k) * o.sz);
                 }
             }
-            *reinterpret_cast<uint4 *>(sm1 + slot * SP1 + 16 * xswz(c)) = make_uint4(v[0], v[1], v[2], v[3]);
+            *reinterpret_cast<uint4 *>(smA + slot * SP1 + 16 * xswz(c)) = make_uint4(v[0], v[1], v[2], v[3]);
         }
-    }
+    };
+
+    // zero area B (f3 rows land on part of it) and the zero chunk; stage block 0; then a cluster
+    // barrier: every CTA of the cluster has started and zeroed before any remote write
+    for (int i = tid; i < SMB / 16 + 1; i += THREADS) reinterpret_cast<uint4 *>(smB)[i] = make_uint4(0u, 0u, 0u, 0u);
+    stage();
     cluster.sync();
 
-    Acc acc[8][R], acc2[4][R];
-    auto zero_acc = [&]() {
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-#pragma unroll
-            for (int j = 0; j < R; ++j) acc[i][j] = Acc(0);
-    };
-    auto zero_acc2 = [&]() {
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < R; ++j) acc2[i][j] = Acc(0);
-    };
-
-    // ---- phase 1 x-step: task (blk, w2, run) -> X(r1, w2) for all 8 r1, written in place
+    Acc acc[8][R1];
     {
-        const int blk = tid / (8 * NRX1), rest = tid % (8 * NRX1), w2 = rest / NRX1, run = rest % NRX1;
-        const bool act = tid < NB * 8 * NRX1;
-        unsigned char *base = sm1 + blk * 64 * SP1;
-        if (act) {
-            zero_acc();
-            drt_accumulate<3, R, SP1, false, Acc>(base, w2, 8, 2 * run, p.one, acc);
-        }
-        __syncthreads();
-        if (act) {
+        // x-step: task (blk, w2, run) -> X(r1, w2) for all 8 r1, written in place over slot (r1, w2)
+        {
+            const int blk = tid / (8 * NRX1), rest = tid % (8 * NRX1), w2 = rest / NRX1, run = rest % NRX1;
+            const bool act = tid < NB * 8 * NRX1;
+            unsigned char *base = smA + blk * 64 * SP1;
+            if (act) {
 #pragma unroll
-            for (int r1 = 0; r1 < 8; ++r1)
+                for (int i = 0; i < 8; ++i)
 #pragma unroll
-                for (int h = 0; h < 2; ++h)
-                    *reinterpret_cast<uint4 *>(base + (r1 * 8 + w2) * SP1 + 16 * xswz(2 * run + h)) =
-                        make_uint4(Lane<Acc>::bits(acc[r1][4 * h]), Lane<Acc>::bits(acc[r1][4 * h + 1]),
-                                   Lane<Acc>::bits(acc[r1][4 * h + 2]), Lane<Acc>::bits(acc[r1][4 * h + 3]));
+                    for (int j = 0; j < R1; ++j) acc[i][j] = Acc(0);
+                drt_accumulate<3, R1, SP1, false, Acc>(base, w2, 8, run, p.one, acc);
+            }
+            __syncthreads();
+            if (act) {
+#pragma unroll
+                for (int r1 = 0; r1 < 8; ++r1)
+                    *reinterpret_cast<uint4 *>(base + (r1 * 8 + w2) * SP1 + 16 * xswz(run)) =
+                        make_uint4(Lane<Acc>::bits(acc[r1][0]), Lane<Acc>::bits(acc[r1][1]),
+                                   Lane<Acc>::bits(acc[r1][2]), Lane<Acc>::bits(acc[r1][3]));
+            }
+            __syncthreads();
         }
-        __syncthreads();
-    }
-    // ---- phase 1 y-step: task (blk, r1, run) -> f3(r1, r2 | V) for all 8 r2, sent to CTA r1
-    {
-        const int blk = tid / (8 * NRY1), rest = tid % (8 * NRY1), r1 = rest / NRY1, run = rest % NRY1;
-        if (tid < NB * 8 * NRY1) {
+        // y-step: task (blk, r1, run), 16 lanes per r1 (12 active) -> f3(r1, r2 | V) for all 8 r2, sent
+        // to CTA r1 as chunks: lane `run` holds f3 elements e = 4 run .. + 3, which land at k = e + shift
+        {
+            const int blk = tid >> 7, r1 = (tid >> 4) & 7, run = tid & 15;
             const int b = NB * q + blk, V1 = b >> 2, V2 = b & 3;
-            zero_acc();
-            drt_accumulate<3, R, SP1, false, Acc>(sm1 + blk * 64 * SP1, r1 * 8, 1, 2 * run, p.one, acc);
-            unsigned char *dst = cluster.map_shared_rank(sm2, r1) + (V1 * 4 + V2) * SP2;
+            const bool act = run < NRY1;
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < R1; ++j) acc[i][j] = Acc(0);
+            if (act) drt_accumulate<3, R1, SP1, false, Acc>(smA + blk * 64 * SP1, r1 * 8, 1, run, p.one, acc);
+            unsigned char *dst = cluster.map_shared_rank(smB, r1) + (V1 * 4 + V2) * RB;
 #pragma unroll
             for (int r2 = 0; r2 < 8; ++r2) {
-                // p = e - 8 + r1 (4 - V1) + r2 (4 - V2) >= 0 wherever f3 can be non-zero (z >= -(r1 + r2))
-                const int p0 = R * run - 8 + r1 * (4 - V1) + r2 * (4 - V2);
-                unsigned char *row = dst + r2 * GROUP_BYTES;
+                uint32_t w[7];
 #pragma unroll
-                for (int j = 0; j < R; ++j)
-                    if (p0 + j >= 0) *reinterpret_cast<uint32_t *>(row + elem_off(p0 + j)) = Lane<Acc>::bits(acc[r2][j]);
+                for (int i = 0; i < 4; ++i) w[i] = Lane<Acc>::bits(acc[r2][i]);
+#pragma unroll
+                for (int i = 0; i < 3; ++i) w[4 + i] = __shfl_down_sync(0xffffffffu, w[i], 1, 16);
+                if (!act) continue;
+                if (run == NRY1 - 1) w[4] = w[5] = w[6] = 0u;        // past e = 48: zeros
+                const int u = 8 - r1 * (4 - V1) - r2 * (4 - V2);
+                const int shift = (4 - (u & 3)) & 3;
+                unsigned char *row = dst + r2 * 16 * RB;
+                if (shift == 0) {
+                    *reinterpret_cast<uint4 *>(row + 16 * xswz(run)) = make_uint4(w[0], w[1], w[2], w[3]);
+                } else {
+                    // chunk run + 1 = elements 4 - shift .. of the window w (own tail, next lane's head)
+                    uint32_t c[4];
+                    const int s = 4 - shift;                                    // 1..3
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const uint32_t a1 = (s & 1) ? w[i + 1] : w[i];
+                        const uint32_t a3 = (s & 1) ? w[i + 3] : w[i + 2];
+                        c[i] = (s & 2) ? a3 : a1;
+                    }
+                    *reinterpret_cast<uint4 *>(row + 16 * xswz(run + 1)) = make_uint4(c[0], c[1], c[2], c[3]);
+                    if (run == 0) {
+                        // chunk 0: `shift` zeros, then the first 4 - shift elements
+                        uint32_t h[4];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const int src = i - shift;
+                            h[i] = src == 0 ? w[0] : src == 1 ? w[1] : src == 2 ? w[2] : 0u;
+                        }
+                        *reinterpret_cast<uint4 *>(row) = make_uint4(h[0], h[1], h[2], h[3]);
+                    }
+                }
             }
         }
     }
     cluster.sync();                                          // every f3 row has arrived
 
-    // ---- phase 2: groups sigma = (q, g), two at a time (task = (group of the pair, V2 | rho1, run))
+    // ---- phase 2: groups sigma = (q, g), GP at a time
     Acc *outp = reinterpret_cast<Acc *>(p.out) + (long long)inst * N * N * 3 * N;
-    for (int g0 = 0; g0 < 8; g0 += 2) {
+    Acc acc2[4][R2];
+    for (int g0 = 0; g0 < 8; g0 += GP) {
         {
+            // x-step: task (group of the pair, V2, run) -> X2(rho1, V2), area A
             const int gp = tid / (4 * NRX2), rest = tid % (4 * NRX2), V2 = rest / NRX2, run = rest % NRX2;
             const int g = g0 + gp;
             const int wout = 40 + 4 * (q + g);
-            const bool act = tid < 2 * 4 * NRX2 && R * run < wout + 3;
-            unsigned char *base = sm2 + g * GROUP_BYTES;
-            if (act) {
-                zero_acc2();
-                drt_accumulate<2, R, SP2, false, Acc>(base, V2, 4, 2 * run, p.one, acc2);
-            }
-            __syncthreads();
-            if (act) {
+            if (tid < GP * 4 * NRX2 && R2 * run < wout + 3) {
+                const unsigned char *rows[4];
+                int co[4];
+#pragma unroll
+                for (int V1 = 0; V1 < 4; ++V1) {
+                    const int u = 8 - q * (4 - V1) - g * (4 - V2);
+                    co[V1] = (u + ((4 - (u & 3)) & 3)) >> 2;               // A / 4 (exact)
+                    rows[V1] = smB + (g * 16 + V1 * 4 + V2) * RB;
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < R2; ++j) acc2[i][j] = Acc(0);
+                acc_rows_b<2, R2, Acc>(rows, co, 2 * run, zero, p.one, acc2);
+                unsigned char *xb = smA + gp * 16 * SPX;
 #pragma unroll
                 for (int rho1 = 0; rho1 < 4; ++rho1)
 #pragma unroll
                     for (int h = 0; h < 2; ++h)
-                        *reinterpret_cast<uint4 *>(base + (rho1 * 4 + V2) * SP2 + 16 * xswz(2 * run + h)) =
+                        *reinterpret_cast<uint4 *>(xb + (rho1 * 4 + V2) * SPX + 16 * xswz(2 * run + h)) =
                             make_uint4(Lane<Acc>::bits(acc2[rho1][4 * h]), Lane<Acc>::bits(acc2[rho1][4 * h + 1]),
                                        Lane<Acc>::bits(acc2[rho1][4 * h + 2]), Lane<Acc>::bits(acc2[rho1][4 * h + 3]));
             }
             __syncthreads();
         }
         {
+            // y-step: task (group of the pair, rho1, run) -> out(4q + rho1, 4g + rho2), rho2 = 0..3
             const int gp = tid / (4 * NRY2), rest = tid % (4 * NRY2), rho1 = rest / NRY2, run = rest % NRY2;
             const int g = g0 + gp;
-            const int ssum = q + g, wout = 40 + 4 * ssum, dz = 56 - 4 * ssum;   // D of stored p = 0
-            if (tid < 2 * 4 * NRY2) {
-                const int s1 = 4 * q + rho1;
-                Acc *orow = outp + ((long long)s1 * N + 4 * g) * (3 * N);
-                if (R * run < wout) {
-                    zero_acc2();
-                    drt_accumulate<2, R, SP2, false, Acc>(sm2 + g * GROUP_BYTES, rho1 * 4, 1, 2 * run, p.one, acc2);
-                    const bool two = R * run + 4 < wout;                // wout is a multiple of 4, not of 8
+            const int ssum = q + g, wout = 40 + 4 * ssum, dz = 56 - 4 * ssum;   // D of p = 0
+            if (tid < GP * 4 * NRY2) {
+                Acc *orow = outp + ((long long)(4 * q + rho1) * N + 4 * g) * (3 * N);
+                if (R2 * run < wout) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < R2; ++j) acc2[i][j] = Acc(0);
+                    drt_accumulate<2, R2, SPX, false, Acc>(smA + gp * 16 * SPX, rho1 * 4, 1, 2 * run, p.one, acc2);
+                    const bool two = R2 * run + 4 < wout;              // wout is a multiple of 4, not of 8
 #pragma unroll
                     for (int rho2 = 0; rho2 < 4; ++rho2) {
-                        Acc *d = orow + rho2 * (3 * N) + dz + R * run;
+                        Acc *d = orow + rho2 * (3 * N) + dz + R2 * run;
                         st_cs_v4(d, Lane<Acc>::bits(acc2[rho2][0]), Lane<Acc>::bits(acc2[rho2][1]),
                                  Lane<Acc>::bits(acc2[rho2][2]), Lane<Acc>::bits(acc2[rho2][3]));
                         if (two)
@@ -209,6 +278,7 @@ drt_small32_kernel(const DrtPass p) {
 #pragma unroll
                     for (int rho2 = 0; rho2 < 4; ++rho2) st_cs_v4(orow + rho2 * (3 * N) + 4 * c, 0u, 0u, 0u, 0u);
             }
+            __syncthreads();                                 // area A is rewritten by the next pair
         }
     }
 }

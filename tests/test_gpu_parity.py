@@ -487,9 +487,11 @@ def test_binding_validates_user_buffers():
     """The binding checks caller-supplied buffers and tells the C ABI their real sizes (no
     writes past a short workspace, no coefficient reads past a buffer with fewer dodecants)."""
     cube = _gpu(synth.uniform_cube(32, 61, np.uint8))
-    need = d3.drt3d_planes_workspace_size(32, 0xFFF, d3.make_opts())
+    big = _gpu(synth.uniform_cube(64, 61, np.uint8))                   # N = 64 has a workspace
+    need = d3.drt3d_planes_workspace_size(64, 0xFFF, d3.make_opts())
+    assert need > 0
     with pytest.raises(d3.Drt3dError):
-        d3.planes(cube, 0xFFF, workspace=torch.empty(need // 2, dtype=torch.uint8, device="cuda"))
+        d3.planes(big, 0xFFF, workspace=torch.empty(need // 2, dtype=torch.uint8, device="cuda"))
     with pytest.raises(d3.Drt3dError):
         d3.planes(cube, 0xFFF, out=torch.empty((12, 32, 32, 95), dtype=torch.int32, device="cuda"))
     with pytest.raises(d3.Drt3dError):
