@@ -173,7 +173,18 @@ drt3d_status make_plan(int transform, int N, uint32_t mask, const drt3d_opts &o,
     P.inst = P.batch * P.ndod;
     // pass radices: <= 4 stages per pass, the first pass takes the larger half
     if (n <= 4) { P.npass = 1; P.ks[0] = n; }
-    else if (n <= 8) { P.npass = 2; P.ks[0] = (n + 1) / 2; P.ks[1] = n / 2; }
+    else if (n <= 8) {
+        P.npass = 2;
+        P.ks[0] = (n + 1) / 2;
+        P.ks[1] = n / 2;
+#ifndef D3_DJT_K1
+#define D3_DJT_K1 0
+#endif
+        if (transform == 1 && D3_DJT_K1 > 0 && D3_DJT_K1 < n && D3_DJT_K1 <= 4 && n - D3_DJT_K1 <= 4) {
+            P.ks[0] = D3_DJT_K1;
+            P.ks[1] = n - D3_DJT_K1;
+        }
+    }
     else { P.npass = 3; P.ks[0] = 4; P.ks[1] = (n - 3) / 2; P.ks[2] = n - 4 - P.ks[1]; }
     P.cs[0] = 0;
     for (int p = 0; p < P.npass; ++p) P.cs[p + 1] = P.cs[p] + P.ks[p];
@@ -225,11 +236,14 @@ drt3d_status make_plan(int transform, int N, uint32_t mask, const drt3d_opts &o,
         }
     }
     P.base[0] = transform == 0 ? 2 * N : N;
-#ifdef D3_SMALL32
-    // measurement builds (-DD3_SMALL32): every stage on chip in one 8-CTA cluster per instance
-    // (k_small.cu), no stage buffers.  Measured slower than the two passes for fp32 and int32
-    // (cfg5: 1.06 vs 0.83 ms, DESIGN.md §5 "On-chip N = 32"), faster for u8 (1.00 vs 1.24 ms).
-    if (transform == 0 && N == 32 && o.layout == DRT3D_LAYOUT_STACKED) {
+#ifndef D3_SMALL32
+#define D3_SMALL32 0
+#endif
+    // every stage on chip in one 8-CTA cluster per instance (k_small.cu), no stage buffers: the
+    // default for u8 voxels at N = 32 (256 cubes x 12 dodecants: 1.00 vs 1.24 ms for the two
+    // passes); measured slower for fp32 and int32 (cfg5: 1.06 vs 0.83 ms, DESIGN.md §5 "On-chip
+    // N = 32"), which keep the two passes unless -DD3_SMALL32=1 (measurement builds)
+    if (transform == 0 && N == 32 && o.layout == DRT3D_LAYOUT_STACKED && (D3_SMALL32 || o.in_dtype == DRT3D_U8)) {
         P.small = 1;
         P.chunk = P.inst;
         P.nset = 1;
@@ -237,7 +251,6 @@ drt3d_status make_plan(int transform, int N, uint32_t mask, const drt3d_opts &o,
         P.nlaunch = 1;
         return DRT3D_OK;
     }
-#endif
     P.width[0] = N;
     size_t per_inst = 0;
     for (int p = 1; p < P.npass; ++p) {

@@ -84,6 +84,21 @@ djt_pass_kernel(const DjtPass p) {
     {
         const int s1max = (sg1 << K) + S - 1, s2max = (sg2 << K) + S - 1;
         if (D1abs + T1 <= N - s1max || D2abs + T2 <= N - s2max) {
+            constexpr int EPV = 16 / (int)sizeof(Out);
+            if (T2 % EPV == 0 && d20 + T2 <= p.out_width && (p.out_pitch * (int)sizeof(Out)) % 16 == 0 &&
+                (d20 * (int)sizeof(Out)) % 16 == 0 && (p.out_plane * (long long)sizeof(Out)) % 16 == 0) {
+                // 16-byte streaming stores; the plane pointer changes every T1 * T2 / EPV chunks
+                constexpr int CPR = T2 / EPV, CPP = T1 * CPR;
+                for (int i = tid; i < S * S * CPP; i += blockDim.x) {
+                    const int pl = i / CPP, rem = i - pl * CPP, e1 = rem / CPR, q = rem - e1 * CPR;
+                    if (d10 + e1 < p.out_width) {
+                        Out *dst = out_plane_ptr(pl / S, pl % S) + (long long)(d10 + e1) * p.out_pitch + d20 + q * EPV;
+                        if (FINAL) st_cs_v4(dst, 0u, 0u, 0u, 0u);
+                        else *reinterpret_cast<uint4 *>(dst) = make_uint4(0u, 0u, 0u, 0u);
+                    }
+                }
+                return;
+            }
             for (int i = tid; i < S * S * T1 * T2; i += blockDim.x) {
                 const int e2 = i % T2, rest = i / T2, e1 = rest % T1, pl = rest / T1;
                 if (d10 + e1 < p.out_width && d20 + e2 < p.out_width)

@@ -113,7 +113,10 @@ template <> struct DjtTile<2> { static constexpr int R = 8, T1 = 8, T2 = 64; };
 #ifndef D3_DJT3_T2
 #define D3_DJT3_T2 32      // swept 16 / 32 / 64 / 128 (T1 = 4 / 8 / 16 / 32): T1 8 x T2 32 best on cfg4
 #endif
-template <> struct DjtTile<3> { static constexpr int R = 8, T1 = D3_DJT3_T1, T2 = D3_DJT3_T2; };
+#ifndef D3_DJT3_R
+#define D3_DJT3_R 8
+#endif
+template <> struct DjtTile<3> { static constexpr int R = D3_DJT3_R, T1 = D3_DJT3_T1, T2 = D3_DJT3_T2; };
 template <> struct DjtTile<4> { static constexpr int R = 8, T1 = 4, T2 = 64; };
 
 template <int K, class In, class Acc, class Out, bool FIRST, bool FINAL>

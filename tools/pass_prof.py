@@ -1,8 +1,8 @@
-"""Per-phase clock accounting of the u16 final pass (debug build libdrt3d_pprof.so)."""
+"""Per-phase clock accounting of the u16 final pass (debug build libdrt3d_ppprof.so)."""
 import ctypes, os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-os.environ["D3_LIB"] = os.path.join(ROOT, "paper_2501_13664_b200", "libdrt3d_pprof.so")
+os.environ["D3_LIB"] = os.path.join(ROOT, "paper_2501_13664_b200", "libdrt3d_ppprof.so")
 import numpy as np, torch
 import paper_2501_13664_b200 as d3, synth
 L = d3.lib()
