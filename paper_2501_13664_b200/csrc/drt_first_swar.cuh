@@ -43,7 +43,11 @@ struct SwarGeom {
 #ifndef SWAR_CTAS
 #define SWAR_CTAS 4
 #endif
-    static constexpr int CTAS = SWAR_CTAS;                // target CTAs per SM (register cap)
+#ifndef SWAR_CTAS3
+#define SWAR_CTAS3 12                 // swept 4 / 8 / 12 / 16 on cfg2: 12 best (0.048 -> 0.044 ms)
+#endif
+    // target CTAs per SM (register cap): K = 4 (96 threads, 51 KB) 4; K = 3 (64 threads, 11 KB) SWAR_CTAS3
+    static constexpr int CTAS = K == 4 ? SWAR_CTAS : SWAR_CTAS3;
     static constexpr int MAXREG0 = 65536 / (CTAS * THREADS) / 8 * 8;
     static constexpr int MAXREG = MAXREG0 > 255 ? 255 : MAXREG0;
     static_assert(T % R == 0 && (R == 8 || R == 4), "tile shape");

@@ -50,7 +50,13 @@ drt3d_status launch_drt_k(const DrtPass &prm_in, int ninst, cudaStream_t st) {
 #endif
     // u16-input final passes use a narrower tile (more resident CTAs per SM); non-final passes keep
     // T / R a power of two (their epilogue shuffles across the T / R runs of a row)
-    constexpr int R = DrtTile<K>::R, T = (!FIRST && FINAL && sizeof(In) == 2 && K == 4) ? D3_FINAL16_T : DrtTile<K>::T;
+#ifndef D3_SINGLE_T
+#define D3_SINGLE_T 64                  // the single-pass plan (N = 16, K = 4): D tile width
+#endif
+    constexpr int R = DrtTile<K>::R,
+                  T = (!FIRST && FINAL && sizeof(In) == 2 && K == 4) ? D3_FINAL16_T
+                      : (FIRST && FINAL && K == 4)                 ? D3_SINGLE_T
+                                                                   : DrtTile<K>::T;
     if constexpr (FIRST && !FINAL && K >= 3 && std::is_same<In, uint8_t>::value && std::is_same<Out, uint16_t>::value) {
         // u8 voxels -> u16 stage-K rows: packed 16-bit lanes (drt_first_swar.cuh)
 #ifndef SWAR_R

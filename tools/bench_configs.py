@@ -151,7 +151,7 @@ def run_apps():
     f = (f + (rng.random((N, N, N)) < 0.005)).astype(np.uint8)
     cube = torch.from_numpy(f).cuda()
     c = d3.planes(cube, 0xFFF)
-    ws = d3._apps_ws(c.device)
+    ws = d3._apps_ws(None, c.device)[0]
     t_fwd = _time(lambda: d3.planes(cube, 0xFFF, out=c))
     t_det = _time(lambda: d3.detect_planes(c, 0xFFF, 1, 3, 1, 10, workspace=ws))
     flags, _ = d3.detect_planes(c, 0xFFF, 1, 3, 1, 10, workspace=ws)

@@ -20,7 +20,7 @@ def main(rep, out):
         acc[d["Kernel Name"]].append(rd + wr)
     res = {k: sum(v) / len(v) for k, v in acc.items()}
     fin = [v for k, v in res.items() if "drt_pass_kernel" in k and ", 0, 1>" in k]
-    j = {"source": rep.split("/")[-1] + " (ncu --set full, default cache control: caches flushed before each launch)",
+    j = {"source": rep.split("/")[-1] + " (ncu --set full --cache-control none --clock-control none)",
          "per_kernel_dram_bytes_per_launch": res,
          "final_pass_dram_bytes_per_launch": fin[0] if fin else None}
     json.dump(j, open(out, "w"), indent=1)
