@@ -29,14 +29,14 @@ inline PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
     return fn;
 }
 
-// 4D map of the stacked DRT output out[inst][s1][s2][3N] (32-bit), box {T, S, S, 1}
-inline bool make_out_map(CUtensorMap *m, void *out, int N, int inst_total, int T, int S) {
+// 4D map of the stacked DRT output out[inst][s1][s2][3N] (32-bit), box {T, S, S1, 1}
+inline bool make_out_map(CUtensorMap *m, void *out, int N, int inst_total, int T, int S, int S1) {
     auto enc = tmap_encoder();
     if (!enc) return false;
     const cuuint64_t W = 3ull * N;
     cuuint64_t dims[4] = {W, (cuuint64_t)N, (cuuint64_t)N, (cuuint64_t)inst_total};
     cuuint64_t str[3] = {W * 4, W * 4 * N, W * 4 * N * N};
-    cuuint32_t box[4] = {(cuuint32_t)T, (cuuint32_t)S, (cuuint32_t)S, 1}, es[4] = {1, 1, 1, 1};
+    cuuint32_t box[4] = {(cuuint32_t)T, (cuuint32_t)S, (cuuint32_t)S1, 1}, es[4] = {1, 1, 1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, out, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
            CUDA_SUCCESS;
@@ -91,7 +91,8 @@ drt3d_status launch_drt_k(const DrtPass &prm_in, int ninst, cudaStream_t st) {
     if constexpr (FINAL && sizeof(Out) == 4) {
         constexpr int S = 1 << K;
         if (!no_tma && prm.layout == 0 && prm.m == 0 && prm.out_width % T == 0 && S * S * T * 4 <= G::SMEM &&
-            make_out_map(&omap, prm.out, prm.N, prm.inst_total, T, S))
+            make_out_map(&omap, prm.out, prm.N, prm.inst_total, T, S,
+                         drt_warp_store<K, R, T, !FIRST && sizeof(In) == 2, FINAL>() ? 4 : S))
             prm.tma_store = 1;
     }
     kern<<<grid, G::THREADS, G::SMEM, st>>>(prm, omap);
