@@ -53,9 +53,13 @@ drt3d_status launch_drt_k(const DrtPass &prm_in, int ninst, cudaStream_t st) {
 #ifndef D3_SINGLE_T
 #define D3_SINGLE_T 64                  // the single-pass plan (N = 16, K = 4): D tile width
 #endif
+#ifndef D3_FINAL2_T
+#define D3_FINAL2_T 96                  // K = 2 final passes: T = 3N at N = 32 (swept 48 / 64 / 96 / 128: cfg5 0.827 -> 0.741 ms)
+#endif
     constexpr int R = DrtTile<K>::R,
                   T = (!FIRST && FINAL && sizeof(In) == 2 && K == 4) ? D3_FINAL16_T
                       : (FIRST && FINAL && K == 4)                 ? D3_SINGLE_T
+                      : (!FIRST && FINAL && K == 2)                ? D3_FINAL2_T
                                                                    : DrtTile<K>::T;
     if constexpr (FIRST && !FINAL && K >= 3 && std::is_same<In, uint8_t>::value && std::is_same<Out, uint16_t>::value) {
         // u8 voxels -> u16 stage-K rows: packed 16-bit lanes (drt_first_swar.cuh)
