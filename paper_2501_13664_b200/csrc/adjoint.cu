@@ -323,18 +323,24 @@ __global__ void __launch_bounds__(256) drt_adj_gather(const T *__restrict__ l0, 
         const int base = (p0 > 0 ? 0 : ((1 << l0e) - 1) * str(a0)) + (p1 > 0 ? 0 : ((1 << l1e) - 1) * str(a1)) +
                          (p2 > 0 ? 0 : ((1 << l2e) - 1) * str(a2));
         const T *src = l0 + (long long)j * l0_stride + ((size_t)o0 * N + o1) * pitch + o2;
-        T v[8];
+        // 16-byte loads along z' (the box extent along z' is 8 or 32, origins are multiples of 8,
+        // the pitch a multiple of 4): item = 4 consecutive z', 2 items per thread
+        const int lq = l2e - 2;
+        uint4 v[2];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < 2; ++i) {
             const int e = tid + 256 * i;
-            const int zo = e & ((1 << l2e) - 1), yo = (e >> l2e) & ((1 << l1e) - 1), xo = e >> (l2e + l1e);
-            v[i] = __ldg(src + ((size_t)xo * N + yo) * pitch + zo);
+            const int zq = e & ((1 << lq) - 1), yo = (e >> lq) & ((1 << l1e) - 1), xo = e >> (lq + l1e);
+            v[i] = __ldg(reinterpret_cast<const uint4 *>(src + ((size_t)xo * N + yo) * pitch + 4 * zq));
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < 2; ++i) {
             const int e = tid + 256 * i;
-            const int zo = e & ((1 << l2e) - 1), yo = (e >> l2e) & ((1 << l1e) - 1), xo = e >> (l2e + l1e);
-            sm[base + xo * m0 + yo * m1 + zo * m2] = v[i];
+            const int zq = e & ((1 << lq) - 1), yo = (e >> lq) & ((1 << l1e) - 1), xo = e >> (lq + l1e);
+            const int b = base + xo * m0 + yo * m1 + 4 * zq * m2;
+            const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) sm[b + k * m2] = Lane<T>::get(w[k]);
         }
         __syncthreads();
 #pragma unroll

@@ -242,8 +242,9 @@ drt3d_status make_plan(int transform, int N, uint32_t mask, const drt3d_opts &o,
     // every stage on chip in one 8-CTA cluster per instance (k_small.cu), no stage buffers: the
     // default for u8 voxels at N = 32 (256 cubes x 12 dodecants: 1.00 vs 1.24 ms for the two
     // passes); measured slower for fp32 and int32 (cfg5: 1.06 vs 0.83 ms, DESIGN.md §5 "On-chip
-    // N = 32"), which keep the two passes unless -DD3_SMALL32=1 (measurement builds)
-    if (transform == 0 && N == 32 && o.layout == DRT3D_LAYOUT_STACKED && (D3_SMALL32 || o.in_dtype == DRT3D_U8)) {
+    // N = 32"), which keep the two passes unless -DD3_SMALL32=1 (measurement builds; 2: never)
+    if (transform == 0 && N == 32 && o.layout == DRT3D_LAYOUT_STACKED && D3_SMALL32 != 2 &&
+        (D3_SMALL32 == 1 || o.in_dtype == DRT3D_U8)) {
         P.small = 1;
         P.chunk = P.inst;
         P.nset = 1;
