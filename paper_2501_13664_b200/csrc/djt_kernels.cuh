@@ -15,6 +15,9 @@
 // stage is out[s1][s2][D1][D2] with Di in [0, 2N) (Alg. 3 + separateS1S2).
 #pragma once
 #include "common.cuh"
+#ifndef D3_FADD2
+#define D3_FADD2 0
+#endif
 
 namespace d3 {
 
@@ -202,8 +205,19 @@ djt_pass_kernel(const DjtPass p) {
             static_for<0, S>([&](auto r_) {
                 constexpr int r = decltype(r_)::value;
                 constexpr int off = lk(K, r, w);
+                if constexpr (std::is_same<Acc, float>::value && D3_FADD2 && R % 2 == 0) {
+                    // fp32: two outputs per instruction (sm_100 FADD2; off by default, drt_kernels.cuh)
 #pragma unroll
-                for (int j = 0; j < R; ++j) acc[r][j] = acc[r][j] + Lane<Acc>::get(buf[j + off]);
+                    for (int j = 0; j < R; j += 2) {
+                        const float2 a = __fadd2_rn(make_float2(acc[r][j], acc[r][j + 1]),
+                                                    make_float2(__uint_as_float(buf[j + off]), __uint_as_float(buf[j + off + 1])));
+                        acc[r][j] = a.x;
+                        acc[r][j + 1] = a.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < R; ++j) acc[r][j] = acc[r][j] + Lane<Acc>::get(buf[j + off]);
+                }
             });
         });
         // store S output planes (r1, r2), row d1, columns run rr

@@ -190,8 +190,23 @@ __device__ __forceinline__ void drt_accumulate(const unsigned char *__restrict__
 #define D3_FMA_LT 1
 #endif
                 constexpr bool fma = FMA16 < 0 ? (r % D3_FMA_MOD) < D3_FMA_LT : fma_row(r, FMA16);
+#ifndef D3_FADD2
+#define D3_FADD2 0                  // measured slower: cfg5 0.758 vs 0.741 ms, N=256 f32 2.03 vs 1.98 ms
+#endif
+                if constexpr (std::is_same<Acc, float>::value && D3_FADD2 && R % 2 == 0) {
+                    // fp32: two outputs per instruction (sm_100 FADD2), same summation order as add2
 #pragma unroll
-                for (int j = 0; j < R; ++j) acc[r][j] = add2<Acc>(acc[r][j], b0[j + o0], b1[j + o1], one, fma);
+                    for (int j = 0; j < R; j += 2) {
+                        float2 a = make_float2(acc[r][j], acc[r][j + 1]);
+                        a = __fadd2_rn(a, make_float2(__uint_as_float(b0[j + o0]), __uint_as_float(b0[j + o0 + 1])));
+                        a = __fadd2_rn(a, make_float2(__uint_as_float(b1[j + o1]), __uint_as_float(b1[j + o1 + 1])));
+                        acc[r][j] = a.x;
+                        acc[r][j + 1] = a.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < R; ++j) acc[r][j] = add2<Acc>(acc[r][j], b0[j + o0], b1[j + o1], one, fma);
+                }
             });
         });
     }
