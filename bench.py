@@ -279,6 +279,13 @@ def run_ours(args):
             tj = json.load(fh)
         traffic, traffic_src = tj.get("final_pass_dram_bytes_per_launch"), tj.get("source")
     share = sum(kind_ms[2]) / max(1e-9, sum(kind_ms[0]) + sum(kind_ms[1]) + sum(kind_ms[2]))
+    # context: the incompressible write-only HBM ceiling measured on this GPU type (the final pass is
+    # ~83% writes), profiles/r2_hbm_ceilings.json (tools/hbm_write_probe.py)
+    wceil = None
+    cpath = os.path.join(ROOT, "profiles", "r2_hbm_ceilings.json")
+    if os.path.exists(cpath):
+        with open(cpath) as fh:
+            wceil = json.load(fh).get("write_only_ceiling_gbs")
 
     # e2e through the host-buffer C entry point (pinned host cube + output)
     e2e = None
@@ -332,7 +339,8 @@ def run_ours(args):
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "traffic_source": traffic_src,
                          "algorithmic_bytes_per_launch": final_bytes, "dodecants_per_launch": dod_per_final_launch,
-                         "launch_ms": fin_ms, "first_pass_ms": first_ms, "share_of_step": share},
+                         "launch_ms": fin_ms, "first_pass_ms": first_ms, "share_of_step": share,
+                         "write_ceiling_gbs": wceil, "frac_of_write_ceiling": achieved / wceil if wceil else None},
             "gpu_launches": launches,
             "clocks": clocks,
             "e2e": e2e,
