@@ -290,6 +290,62 @@ drt_first_swar_kernel(const DrtPass p) {
 #ifdef D3_PROF_SWAR
         if (step == 0) SW_MARK(2); else SW_MARK(4);
 #endif
+#ifndef D3_SWAR_DIRECT
+#define D3_SWAR_DIRECT 0                 // measured: first pass 0.691 ms vs 0.451 with the unpack + copy-out
+#endif
+        if constexpr (D3_SWAR_DIRECT && G::NRY == 8 && R == 8) {
+            if (step == 1) {
+                // y-step results straight to the stage-K rows (no unpack / copy-out round trip through
+                // shared memory): rows (grp, r2) and (grp + H2, r2), run `run` (8 elements = one
+                // 16-byte chunk), stored pre-shifted by rho (common.cuh) after a one-lane shuffle with
+                // the next run; the 8 runs of a row are 8 consecutive lanes, all lanes of a warp active
+                static_assert(G::YT % 32 == 0, "y-step tasks fill whole warps");
+                if (act) {
+                    uint16_t *outp = reinterpret_cast<uint16_t *>(p.out);
+                    const long long out_inst = (long long)li * p.out_inst_stride;
+                    const int mK = (1 << p.next_k) - 1;
+                    const int wv1 = V1 & mK, wv2 = V2 & mK;
+                    const int e0 = run * R;
+#pragma unroll
+                    for (int r2 = 0; r2 < S; ++r2) {
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const uint32_t sel = h ? 0x7632u : 0x5410u;
+                            const int r1 = grp + h * H2;
+                            uint32_t win[8];
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) win[i] = __byte_perm(acc[r2][2 * i], acc[r2][2 * i + 1], sel);
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) win[4 + i] = __shfl_down_sync(0xffffffffu, win[i], 1, 8);
+                            const int rho = (r1 * wv1 + r2 * wv2) & 7;
+                            const long long row = ((((long long)r1 << K) + r2) << (2 * m)) + ((long long)V1 << m) + V2;
+                            uint16_t *dst = outp + out_inst + row * p.out_pitch + d0 + e0;
+                            uint32_t v[4];
+                            window_chunk<2>(win, rho, 0, v);
+                            if (d0 + e0 < p.out_width) {
+                                if (run == G::NRY - 1) store_chunk_head<2>(dst, v, 8 - rho);
+                                else *reinterpret_cast<uint4 *>(dst) = make_uint4(v[0], v[1], v[2], v[3]);
+                            }
+                            if (run == 0 && rho > 0 && d0 >= 8) {
+                                // tile elements [0, rho) end the previous chunk (whose head the previous tile wrote)
+                                uint32_t tw[8] = {0u, 0u, 0u, 0u, win[0], win[1], win[2], win[3]};
+                                window_chunk<2>(tw, rho, 0, v);
+                                store_chunk_tail<2>(dst - 8, v, rho);
+                            }
+                        }
+                    }
+                }
+#ifdef D3_PROF_SWAR
+                SW_MARK(5);
+                SW_MARK(6);
+                if (tid == 0) {
+                    for (int i = 0; i < 6; ++i) atomicAdd(&d3_swar_prof[i], (unsigned long long)(sw_t[i + 1] - sw_t[i]));
+                    atomicAdd(&d3_swar_prof[7], 1ull);
+                }
+#endif
+                return;
+            }
+        }
         __syncthreads();
         if (act) {
             if (step == 0) {
