@@ -124,6 +124,9 @@ const size_t kChunkBudget = (size_t)D3_CHUNK_MB << 20;
 #ifndef D3_FINAL_PRIORITY
 #define D3_FINAL_PRIORITY 0
 #endif
+#ifndef D3_ZERO_BY_FIRST
+#define D3_ZERO_BY_FIRST 0          // measured: 1.2213 ms per cfg3 step vs 1.1488 with the final pass's own TMA zero tiles
+#endif
 #ifndef D3_OVERLAP_MIN_N
 #define D3_OVERLAP_MIN_N 128
 #endif
@@ -449,6 +452,11 @@ drt3d_status run_drt(const void *cube, uint32_t mask, void *out, const drt3d_opt
     if (ax && (cudaEventRecord(ax->start, st) != cudaSuccess || cudaStreamWaitEvent(ax->a, ax->start, 0) != cudaSuccess))
         return DRT3D_ERR_CUDA;
     JoinGuard join{st, ax ? ax->a : nullptr, ax ? ax->join : nullptr};
+    // -DD3_ZERO_BY_FIRST=1 (measurement builds): for u8 voxels, plan 4 | 4 (N = 256), stacked, the
+    // final pass's all-zero tiles are written by the first pass (one TMA store of a zeroed
+    // shared-memory tile each, DESIGN.md §5 item 6), and the final pass skips them
+    const bool zfirst = D3_ZERO_BY_FIRST && o.in_dtype == DRT3D_U8 && o.layout == DRT3D_LAYOUT_STACKED &&
+                        P.npass == 2 && P.ks[0] == 4 && P.ks[1] == 4 && (3 * P.N) % D3_FINAL16_T == 0;
     const long long final_inst = (o.layout == DRT3D_LAYOUT_MOSAIC) ? 0 : (long long)P.N * P.N * 3 * P.N;
     int chunk_idx = 0;
     for (int i0 = 0; i0 < P.inst; i0 += P.chunk, ++chunk_idx) {
@@ -484,6 +492,12 @@ drt3d_status run_drt(const void *cube, uint32_t mask, void *out, const drt3d_opt
                 prm.out_base = P.base[p + 1];
                 prm.out_width = P.width[p + 1];
                 prm.next_k = fin ? 0 : P.ks[p + 1];
+                if (zfirst && first) {
+                    prm.zf_T = D3_FINAL16_T;
+                    prm.zf_out = out;
+                    prm.zf_inst_stride = final_inst;
+                }
+                if (zfirst && fin) prm.zeros_by_first = 1;
                 drt3d_status s = DRT3D_OK;
                 drt3d_status ls = L.run_on(ps, first ? 0 : (fin ? 2 : 1), [&] {
                     s = dispatch_drt(o.in_dtype, P.ks[p], P.stor[p], P.stor[p + 1], first, fin, prm, gn, ps);

@@ -281,6 +281,12 @@ struct Orient {
 
 constexpr int kMaxDod = 12;
 
+// D tile width of the u16-input K = 4 final pass (the cfg3 kernel, launch.cuh); also the tile grid
+// of the zero tiles the first pass writes for it (api.cu)
+#ifndef D3_FINAL16_T
+#define D3_FINAL16_T 48                 // 3 CTAs/SM (70 KB, 128 threads at 168 registers); 64: 2 CTAs/SM, 3.5% slower
+#endif
+
 enum Stor { ST_U8 = 0, ST_U16 = 1, ST_U32 = 2, ST_F32 = 3 };
 
 }  // namespace d3

@@ -112,7 +112,7 @@ template <int S> __device__ __forceinline__ int copy_row(int i) {
 
 template <int K, int R, int T>
 __global__ void __launch_bounds__(SwarGeom<K, R, T>::THREADS) __maxnreg__((SwarGeom<K, R, T>::MAXREG))
-drt_first_swar_kernel(const DrtPass p) {
+drt_first_swar_kernel(const DrtPass p, const __grid_constant__ CUtensorMap zmap) {
     using G = SwarGeom<K, R, T>;
     constexpr int S = G::S, H2 = G::H2, SP = G::SP, BW = G::BW;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -450,6 +450,35 @@ drt_first_swar_kernel(const DrtPass p) {
             uint32_t tw[8] = {0u, 0u, 0u, 0u, r0[0], r0[1], r0[2], r0[3]}, v[4];
             window_chunk<2>(tw, rho, 0, v);
             store_chunk_tail<2>(dst - 8, v, rho);
+        }
+    }
+    // ---- zero tiles of the final output (DESIGN.md §5 item 6).  This pass leaves HBM mostly idle,
+    // so it stores the final pass's all-zero tiles: its shared memory is free after the copy-out,
+    // a zeroed S x S x zf_T image leaves with one TMA tensor store per tile (zmap: the final output
+    // out[inst][s1][s2][3N], box {zf_T, S, S, 1}).  The final pass has one group per S x S slope
+    // block (sg1, sg2) = (g >> K, g & (S - 1)) -- as many as this pass's column blocks, so this
+    // CTA's g -- and tiles of zf_T along D (out_base 0); tile t is zero when (t + 1) zf_T <=
+    // 2N - s1max - s2max (the final pass's test).  Tiles t = blockIdx.x, + gridDim.x, ... here.
+    if (p.zf_T > 0) {
+        const int gs2 = g & (S - 1), gs1 = g >> K;
+        const int nz = (2 * N - ((gs1 << K) + S - 1) - ((gs2 << K) + S - 1)) / p.zf_T;
+        if ((int)blockIdx.x < nz) {
+            static_assert(K != 4 || G::SMEM >= S * S * D3_FINAL16_T * 4, "a zero tile image fits the shared memory");
+            __syncthreads();                                  // every copy-out read is done
+            for (int i = tid; i < S * S * p.zf_T / 4; i += blockDim.x)
+                reinterpret_cast<uint4 *>(sm)[i] = make_uint4(0u, 0u, 0u, 0u);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            if (tid == 0) {
+                const uint32_t src = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+                for (int t = blockIdx.x; t < nz; t += gridDim.x)
+                    asm volatile(
+                        "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(&zmap),
+                        "r"(t * p.zf_T), "r"(gs2 << K), "r"(gs1 << K), "r"(p.inst0 + li), "r"(src)
+                        : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            }
         }
     }
 #ifdef D3_PROF_SWAR

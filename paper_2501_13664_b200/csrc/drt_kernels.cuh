@@ -59,6 +59,13 @@ struct DrtPass {
     int inst_total;                 // instances (cubes x dodecants) of the whole call
     int tma_store;                  // final pass: emit the output tile with one TMA tensor store
     uint32_t one;                   // = 1; a runtime multiplier so some adds issue as IMAD (FMA pipe)
+    // zero tiles of the final output written by the first pass (DESIGN.md §5 item 6): the first
+    // pass (zf_T > 0) writes the final pass's tiles of width zf_T that lie wholly below the support
+    // into zf_out; the final pass (zeros_by_first) then skips them
+    int zf_T;
+    void *zf_out;
+    long long zf_inst_stride;
+    int zeros_by_first;
     Orient ori[kMaxDod];            // first pass: per-dodecant-slot orientation
     int8_t out_order[kMaxDod][2];   // mosaic: OutOrder[k][0..1]
     int8_t coords[kMaxDod][2];      // mosaic: DodecantCoords[k]
@@ -273,6 +280,30 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
     if constexpr (FINAL) {
         const int s1max = (sg1 << K) + S - 1, s2max = (sg2 << K) + S - 1;
         if (Dabs + T <= 2 * N - s1max - s2max) {
+            if (p.zeros_by_first) return;                // already written by the first pass
+#ifndef D3_ZERO_TMA
+#define D3_ZERO_TMA 1
+#endif
+            if constexpr (sizeof(Out) == 4 && D3_ZERO_TMA && !drt_warp_store<K, R, T, STAGE16, FINAL>()) {
+                if (p.tma_store) {
+                    // a zeroed shared-memory image of the tile leaves with one TMA tensor store (the
+                    // CTA is done once the TMA engine has read it) instead of S*S*T/4 16-byte stores
+                    for (int i = tid; i < S * S * T / 4; i += blockDim.x)
+                        reinterpret_cast<uint4 *>(sm)[i] = make_uint4(0u, 0u, 0u, 0u);
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncthreads();
+                    if (tid == 0) {
+                        const uint32_t src = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+                        asm volatile(
+                            "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(&omap),
+                            "r"(d0), "r"(sg2 << K), "r"(sg1 << K), "r"(inst), "r"(src)
+                            : "memory");
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    }
+                    return;
+                }
+            }
             constexpr int EPV = 16 / (int)sizeof(Out);
             const bool vz = !mosaic && ((p.out_pitch * (int)sizeof(Out)) % 16 == 0) &&
                             ((d0 * (int)sizeof(Out)) % 16 == 0) && (d0 + T <= p.out_width);

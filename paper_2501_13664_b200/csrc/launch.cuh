@@ -45,9 +45,6 @@ inline bool make_out_map(CUtensorMap *m, void *out, int N, int inst_total, int T
 template <int K, class In, class Acc, class Out, bool FIRST, bool FINAL>
 drt3d_status launch_drt_k(const DrtPass &prm_in, int ninst, cudaStream_t st) {
     DrtPass prm = prm_in;
-#ifndef D3_FINAL16_T
-#define D3_FINAL16_T 48                 // 3 CTAs/SM (70 KB, 128 threads at 168 registers); 64: 2 CTAs/SM, 3.5% slower
-#endif
     // u16-input final passes use a narrower tile (more resident CTAs per SM); non-final passes keep
     // T / R a power of two (their epilogue shuffles across the T / R runs of a row)
 #ifndef D3_SINGLE_T
@@ -73,7 +70,14 @@ drt3d_status launch_drt_k(const DrtPass &prm_in, int ninst, cudaStream_t st) {
         if (!set_smem_once(kern, SG::SMEM, smem_done)) return DRT3D_ERR_CUDA;
         const int ntiles = (prm.out_width + 8 + T - 1) / T;
         dim3 grid(ntiles, (unsigned)(1LL << (2 * prm.m)), ninst);
-        kern<<<grid, SG::THREADS, SG::SMEM, st>>>(prm);
+        // the final pass's zero tiles (api.cu, DESIGN.md §5 item 6): map of the final output
+        CUtensorMap zmap;
+        std::memset(&zmap, 0, sizeof(zmap));
+        DrtPass q = prm;
+        if (q.zf_T > 0 && !(K == 4 && q.zf_T == D3_FINAL16_T &&
+                            make_out_map(&zmap, q.zf_out, q.N, q.inst_total, q.zf_T, 1 << K, 1 << K)))
+            return DRT3D_ERR_UNSUPPORTED;
+        kern<<<grid, SG::THREADS, SG::SMEM, st>>>(q, zmap);
         return DRT3D_OK;
     }
     using G = DrtGeom<K, R, T, !FIRST && sizeof(In) == 2>;
