@@ -534,6 +534,7 @@ drt3d_status run_djt(const void *cube, uint32_t mask, void *out, const drt3d_opt
     base.n = P.n;
     base.ndod = P.ndod;
     base.vec_ok = (P.N >= 16) ? 1 : 0;
+    base.inst_total = P.inst;
     int j = 0;
     for (int k = 0; k < 12; ++k)
         if ((mask >> k) & 1) base.ori[j++] = make_orient(rows[k], P.N, k);

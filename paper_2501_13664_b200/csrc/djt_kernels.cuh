@@ -14,6 +14,7 @@
 // Stage 0 is the oriented cube (x' = v, D1 = y' + N, D2 = z' + N), the final
 // stage is out[s1][s2][D1][D2] with Di in [0, 2N) (Alg. 3 + separateS1S2).
 #pragma once
+#include <cuda.h>
 #include "common.cuh"
 #ifndef D3_FADD2
 #define D3_FADD2 0
@@ -32,6 +33,8 @@ struct DjtPass {
     int nt2;                               // tiles along D2
     int inst0, ndod;
     int vec_ok;                            // first pass: 16-byte chunked cube loads are aligned
+    int zero_tma;                          // final pass: zero tiles leave as TMA stores (zmap)
+    int inst_total;                        // instances of the whole call
     Orient ori[kMaxDod];
 };
 
@@ -50,7 +53,15 @@ struct DjtGeom {
 #define D3_DJT_THREADS 128    // 4 CTAs per SM at ~100 registers; 256 (2 per SM) is 1.7% slower on cfg4
 #endif
     static constexpr int THREADS = D3_DJT_THREADS;
-    static constexpr int SMEM = S * WR * PJ * 4;
+    static constexpr int SMEM_STAGE = S * WR * PJ * 4;
+    // final passes with TMA output stores (D3_DJT_OUT_TMA): one S x T1 x T2 32-bit image per warp
+    // behind the staged planes; a warp's 32 tasks of one iteration are exactly one r1
+#ifndef D3_DJT_OUT_TMA
+#define D3_DJT_OUT_TMA 0                  // measured: cfg4 0.0891 vs 0.0860 ms with the direct 16-byte stores
+#endif
+    static constexpr bool OUT_TMA = D3_DJT_OUT_TMA && T1 * NR == 32 && THREADS % 32 == 0 && R == 8;
+    static constexpr int IMG = S * T1 * T2 * 4;
+    static constexpr int SMEM = SMEM_STAGE + (OUT_TMA ? (THREADS / 32) * IMG : 0);
     static_assert(T2 % R == 0 && R % 4 == 0, "tile shape");
 };
 
@@ -59,7 +70,7 @@ struct DjtGeom {
 #endif
 template <int K, int R, int T1, int T2, class In, class Acc, class Out, bool FIRST, bool FINAL>
 __global__ void __launch_bounds__(D3_DJT_THREADS, D3_DJT_MINB)
-djt_pass_kernel(const DjtPass p) {
+djt_pass_kernel(const DjtPass p, const __grid_constant__ CUtensorMap zmap) {
     using G = DjtGeom<K, R, T1, T2>;
     constexpr int S = G::S, WR = G::WR, WC = G::WC, PJ = G::PJ, NR = G::NR;
     extern __shared__ uint4 smem_u4[];
@@ -87,6 +98,27 @@ djt_pass_kernel(const DjtPass p) {
     {
         const int s1max = (sg1 << K) + S - 1, s2max = (sg2 << K) + S - 1;
         if (D1abs + T1 <= N - s1max || D2abs + T2 <= N - s2max) {
+            if constexpr (FINAL && sizeof(Out) == 4) {
+                if (p.zero_tma) {
+                    // S TMA tensor stores of one zeroed S x T1 x T2 shared-memory image (zmap: the final
+                    // output [inst][s1][s2][D1][D2], box {T2, T1, S, 1, 1}); the CTA is done once the TMA
+                    // engine has read it
+                    for (int i = tid; i < S * T1 * T2 / 4; i += blockDim.x) smem_u4[i] = make_uint4(0u, 0u, 0u, 0u);
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncthreads();
+                    if (tid == 0) {
+                        const uint32_t src = static_cast<uint32_t>(__cvta_generic_to_shared(smem_u4));
+                        for (int r1 = 0; r1 < S; ++r1)
+                            asm volatile(
+                                "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(&zmap),
+                                "r"(d20), "r"(d10), "r"(sg2 << K), "r"((sg1 << K) + r1), "r"(inst), "r"(src)
+                                : "memory");
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    }
+                    return;
+                }
+            }
             constexpr int EPV = 16 / (int)sizeof(Out);
             if (T2 % EPV == 0 && d20 + T2 <= p.out_width && (p.out_pitch * (int)sizeof(Out)) % 16 == 0 &&
                 (d20 * (int)sizeof(Out)) % 16 == 0 && (p.out_plane * (long long)sizeof(Out)) % 16 == 0) {
@@ -220,6 +252,34 @@ djt_pass_kernel(const DjtPass p) {
                 }
             });
         });
+        if constexpr (FINAL && sizeof(Out) == 4 && G::OUT_TMA) {
+            if (p.zero_tma) {
+                // this warp's tasks = one r1: its S x T1 x T2 outputs go to the warp's image, then one
+                // TMA tensor store (zmap, box {T2, T1, S, 1, 1}); the image is reused next iteration
+                // after lane 0 has waited for the TMA engine to read it
+                unsigned char *img = reinterpret_cast<unsigned char *>(smem_u4) + G::SMEM_STAGE + (tid >> 5) * G::IMG;
+#pragma unroll
+                for (int r2 = 0; r2 < S; ++r2)
+#pragma unroll
+                    for (int q = 0; q < R / 4; ++q)
+                        *reinterpret_cast<uint4 *>(img + ((r2 * T1 + d1) * T2 + rr * R + 4 * q) * 4) =
+                            make_uint4(Lane<Acc>::bits(acc[r2][4 * q]), Lane<Acc>::bits(acc[r2][4 * q + 1]),
+                                       Lane<Acc>::bits(acc[r2][4 * q + 2]), Lane<Acc>::bits(acc[r2][4 * q + 3]));
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if ((tid & 31) == 0) {
+                    const uint32_t src = static_cast<uint32_t>(__cvta_generic_to_shared(img));
+                    asm volatile(
+                        "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(&zmap),
+                        "r"(d20), "r"(d10), "r"(sg2 << K), "r"((sg1 << K) + r1), "r"(inst), "r"(src)
+                        : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                }
+                __syncwarp();
+                continue;
+            }
+        }
         // store S output planes (r1, r2), row d1, columns run rr
         const int e1 = d10 + d1, e2 = d20 + rr * R;
         if (e1 < p.out_width) {

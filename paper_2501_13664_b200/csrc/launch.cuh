@@ -149,7 +149,29 @@ drt3d_status launch_djt_k(DjtPass prm, int ninst, cudaStream_t st) {
     prm.nt2 = nt2;
     const long long groups = (1LL << (2 * prm.c)) << prm.m;
     dim3 grid(nt1 * nt2, (unsigned)groups, ninst);
-    kern<<<grid, G::THREADS, G::SMEM, st>>>(prm);
+    // final pass: a 5D map of the output [inst][s1][s2][D1][D2] for the zero tiles' TMA stores
+    CUtensorMap zmap;
+    std::memset(&zmap, 0, sizeof(zmap));
+    prm.zero_tma = 0;
+#ifndef D3_DJT_ZERO_TMA
+#define D3_DJT_ZERO_TMA 1
+#endif
+    if constexpr (FINAL && sizeof(Out) == 4) {
+        constexpr int S = 1 << K;
+        if (D3_DJT_ZERO_TMA && prm.m == 0 && prm.out_width % T1 == 0 && prm.out_width % T2 == 0 &&
+            S * T1 * T2 * 4 <= G::SMEM && prm.inst_total > 0) {
+            auto enc = tmap_encoder();
+            const cuuint64_t W = (cuuint64_t)prm.out_width, Nn = (cuuint64_t)prm.N;
+            cuuint64_t dims[5] = {W, W, Nn, Nn, (cuuint64_t)prm.inst_total};
+            cuuint64_t str[4] = {W * 4, W * W * 4, W * W * 4 * Nn, W * W * 4 * Nn * Nn};
+            cuuint32_t box[5] = {(cuuint32_t)T2, (cuuint32_t)T1, (cuuint32_t)S, 1, 1}, es[5] = {1, 1, 1, 1, 1};
+            if (enc && enc(&zmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 5, prm.out, dims, str, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+                prm.zero_tma = 1;
+        }
+    }
+    kern<<<grid, G::THREADS, G::SMEM, st>>>(prm, zmap);
     return DRT3D_OK;
 }
 
