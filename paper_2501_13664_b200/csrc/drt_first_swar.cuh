@@ -397,6 +397,45 @@ drt_first_swar_kernel(const DrtPass p, const __grid_constant__ CUtensorMap zmap)
     const int mK = (1 << p.next_k) - 1;
     const int wv1 = V1 & mK, wv2 = V2 & mK;
     constexpr int NCK = T / 8;
+#ifndef D3_SWAR_COPY_CHUNK
+#define D3_SWAR_COPY_CHUNK 0              // measured: first pass 0.4575 ms vs 0.4514 with one row per thread
+#endif
+#if D3_SWAR_COPY_CHUNK
+    // one 16-byte chunk per item, 8 consecutive lanes per row: every store instruction of a warp
+    // writes 4 whole 128-byte row segments; a lane reads its chunk's 5 words at the rho/2 word offset
+    // (no select network) and the k = 0 lane also writes the tail chunk before the tile
+    for (int it = tid; it < S * S * NCK; it += blockDim.x) {
+        const int rr = it / NCK, k = it - rr * NCK;
+        const int r1 = rr >> K, r2 = rr & (S - 1);
+        const int rho = (r1 * wv1 + r2 * wv2) & 7;
+        const long long row = ((((long long)r1 << K) + r2) << (2 * m)) + ((long long)V1 << m) + V2;
+        uint16_t *dst = outp + out_inst + row * p.out_pitch + d0 + 8 * k;
+        const uint32_t *srow = reinterpret_cast<const uint32_t *>(sm + G::ORP * rr) + row_skew<S>(r1);
+        static_assert(G::SMEM0 >= S * S * G::ORP + 4 * 51 + 12, "skewed rows + chunk overrun");
+        if (d0 + 8 * k < p.out_width) {
+            const int w0 = 4 * k + (rho >> 1);
+            uint32_t w[5];
+#pragma unroll
+            for (int i = 0; i < 5; ++i) w[i] = srow[w0 + i];     // up to 3 words past the row: staging area
+            const uint32_t sel = (rho & 1) ? 0x5432u : 0x3210u;
+            uint32_t v[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v[i] = __byte_perm(w[i], w[i + 1], sel);
+            if (k == NCK - 1) store_chunk_head<2>(dst, v, 8 - rho);
+#ifdef D3_STAGE_EVICT_LAST
+            else st_hint_v4(dst, v[0], v[1], v[2], v[3], keep_pol);
+#else
+            else *reinterpret_cast<uint4 *>(dst) = make_uint4(v[0], v[1], v[2], v[3]);
+#endif
+        }
+        if (k == 0 && rho > 0 && d0 >= 8) {
+            // tile elements [0, rho) end the previous chunk: window (zeros, row words 0..3)
+            uint32_t tw[8] = {0u, 0u, 0u, 0u, srow[0], srow[1], srow[2], srow[3]}, v[4];
+            window_chunk<2>(tw, rho, 0, v);
+            store_chunk_tail<2>(dst - 8, v, rho);
+        }
+    }
+#else
     for (int ii = tid; ii < S * S; ii += blockDim.x) {
         const int rr = copy_row<S>(ii);
         const int r1 = rr >> K, r2 = rr & (S - 1);
@@ -452,6 +491,7 @@ drt_first_swar_kernel(const DrtPass p, const __grid_constant__ CUtensorMap zmap)
             store_chunk_tail<2>(dst - 8, v, rho);
         }
     }
+#endif
     // ---- zero tiles of the final output (DESIGN.md §5 item 6).  This pass leaves HBM mostly idle,
     // so it stores the final pass's all-zero tiles: its shared memory is free after the copy-out,
     // a zeroed S x S x zf_T image leaves with one TMA tensor store per tile (zmap: the final output
