@@ -369,6 +369,15 @@ bool aux_create(Aux &x) {
     return e;
 }
 
+void aux_destroy(Aux &x) {
+    for (cudaStream_t sh : {x.a, x.cp})
+        if (sh) cudaStreamDestroy(sh);
+    for (cudaEvent_t ev : {x.start, x.fdone, x.join, x.cdone[0], x.cdone[1], x.cpdone})
+        if (ev) cudaEventDestroy(ev);
+    for (int g = 0; g < kHostGroups; ++g)
+        if (x.gdone[g]) cudaEventDestroy(x.gdone[g]);
+}
+
 class AuxLease {
     Aux *x_ = nullptr;
 public:
@@ -382,7 +391,11 @@ public:
         if (!x_) {
             Aux *c = new Aux();
             c->dev = dev;
-            if (!aux_create(*c)) { delete c; return; }   // (partially created handles are not reused)
+            if (!aux_create(*c)) {                          // release what was created, run without
+                aux_destroy(*c);
+                delete c;
+                return;
+            }
             g_aux.push_back(c);
             x_ = c;
         }
