@@ -175,7 +175,15 @@ drt3d_status make_plan(int transform, int N, uint32_t mask, const drt3d_opts &o,
     P.ndod = popcount12(mask);
     P.inst = P.batch * P.ndod;
     // pass radices: <= 4 stages per pass, the first pass takes the larger half
-    if (n <= 4) { P.npass = 1; P.ks[0] = n; }
+#ifndef D3_N16_TWO_PASS_MAX_INST
+#define D3_N16_TWO_PASS_MAX_INST 24
+#endif
+    // N = 16 with few instances (one cube, up to 2 x 12 dodecants): two radix-4 passes instead of one
+    // radix-16 pass -- a few large CTAs of the radix-16 kernel are latency-bound (cfg1: 0.0195 ->
+    // 0.0132 ms, one cube x 12 dodecants 0.0174 -> 0.0133 ms); large batches keep the single pass
+    // (no intermediate: 64 fp32 cubes x 12 0.046 vs 0.064 ms)
+    if (transform == 0 && n == 4 && P.inst <= D3_N16_TWO_PASS_MAX_INST) { P.npass = 2; P.ks[0] = 2; P.ks[1] = 2; }
+    else if (n <= 4) { P.npass = 1; P.ks[0] = n; }
     else if (n <= 8) {
         P.npass = 2;
         P.ks[0] = (n + 1) / 2;
