@@ -195,6 +195,23 @@ drt3d_status make_plan(int transform, int N, uint32_t mask, const drt3d_opts &o,
             P.ks[0] = D3_DJT_K1;
             P.ks[1] = n - D3_DJT_K1;
         }
+#ifndef D3_DRT6_K1_U8
+#define D3_DRT6_K1_U8 4
+#endif
+        // u8 voxels at N = 64: the SWAR radix-16 first pass (two 16-bit lanes per add) does more of
+        // the work, 4 | 2 instead of 3 | 3 (cfg2 0.0461 -> 0.0358 ms; 2 | 4: 0.042); fp32 / int32
+        // keep 3 | 3 (8 fp32 cubes x 12: 0.198 ms vs 0.259 at 4 | 2)
+#ifndef D3_PLAN_K1
+#define D3_PLAN_K1 0                    // measurement builds: first-pass radix of every 2-pass plan
+#endif
+        if (D3_PLAN_K1 > 0 && D3_PLAN_K1 < n && D3_PLAN_K1 <= 4 && n - D3_PLAN_K1 <= 4) {
+            P.ks[0] = D3_PLAN_K1;
+            P.ks[1] = n - D3_PLAN_K1;
+        } else if (transform == 0 && n == 6 && o.in_dtype == DRT3D_U8 && D3_DRT6_K1_U8 > 0 && D3_DRT6_K1_U8 <= 4 &&
+            n - D3_DRT6_K1_U8 <= 4) {
+            P.ks[0] = D3_DRT6_K1_U8;
+            P.ks[1] = n - D3_DRT6_K1_U8;
+        }
     }
     else { P.npass = 3; P.ks[0] = 4; P.ks[1] = (n - 3) / 2; P.ks[2] = n - 4 - P.ks[1]; }
     P.cs[0] = 0;
