@@ -53,8 +53,12 @@ drt3d_status launch_drt_k(const DrtPass &prm_in, int ninst, cudaStream_t st) {
 #ifndef D3_FINAL2_T
 #define D3_FINAL2_T 96                  // K = 2 final passes: T = 3N at N = 32 (swept 48 / 64 / 96 / 128: cfg5 0.827 -> 0.741 ms)
 #endif
+#ifndef D3_FINAL16K3_T
+#define D3_FINAL16K3_T 64               // u16-input K = 3 final passes (u8 voxels, N = 128)
+#endif
     constexpr int R = DrtTile<K>::R,
                   T = (!FIRST && FINAL && sizeof(In) == 2 && K == 4) ? D3_FINAL16_T
+                      : (!FIRST && FINAL && sizeof(In) == 2 && K == 3) ? D3_FINAL16K3_T
                       : (FIRST && FINAL && K == 4)                 ? D3_SINGLE_T
                       : (!FIRST && FINAL && K == 2)                ? D3_FINAL2_T
                                                                    : DrtTile<K>::T;
