@@ -122,6 +122,12 @@ drt_first_swar_kernel(const DrtPass p, const __grid_constant__ CUtensorMap zmap)
     const int tile = blockIdx.x, g = blockIdx.y, li = blockIdx.z;
     const int inst = p.inst0 + li;
     const int m = p.m;                                    // c = 0: the group is (V1, V2) only
+#ifndef D3_PDL
+#define D3_PDL 1
+#endif
+    // the dependent final pass may be scheduled from now on (it waits for this grid's completion
+    // before reading the stage buffer: griddepcontrol.wait in drt_pass_kernel)
+    if (D3_PDL) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int V2 = g & ((1 << m) - 1);
     const int V1 = (g >> m) & ((1 << m) - 1);
     const int d0 = tile * T;

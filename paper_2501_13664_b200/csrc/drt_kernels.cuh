@@ -329,6 +329,13 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
     const bool pp_on = tid == 0 && STAGE16 && FINAL;
     long long pp_t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #endif
+#ifndef D3_PDL
+#define D3_PDL 1
+#endif
+    // programmatic dependent launch (DESIGN.md §5 item 8): a final pass may be scheduled while the
+    // pass that writes its input finishes; zero tiles (above) need nothing from it, the rest wait
+    // here until that grid has completed and its writes are visible (a no-op without PDL)
+    if constexpr (!FIRST && D3_PDL) asm volatile("griddepcontrol.wait;" ::: "memory");
     PP_MARK(0);
     // ---- stage the 4^K input rows of the group (32-bit lanes, BW elements per slot)
     auto put = [&](int slot, int e, uint32_t bits) {

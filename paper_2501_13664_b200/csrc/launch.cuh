@@ -107,6 +107,21 @@ drt3d_status launch_drt_k(const DrtPass &prm_in, int ninst, cudaStream_t st) {
                          drt_warp_store<K, R, T, !FIRST && sizeof(In) == 2, FINAL>() ? 4 : S))
             prm.tma_store = 1;
     }
+    if constexpr (!FIRST && D3_PDL) {
+        // programmatic dependent launch: scheduled while the previous kernel on the stream finishes
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(G::THREADS);
+        cfg.dynamicSmemBytes = G::SMEM;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&cfg, kern, prm, omap) != cudaSuccess) return DRT3D_ERR_CUDA;
+        return DRT3D_OK;
+    }
     kern<<<grid, G::THREADS, G::SMEM, st>>>(prm, omap);
     return DRT3D_OK;
 }
