@@ -19,6 +19,9 @@
 #ifndef D3_FADD2
 #define D3_FADD2 0
 #endif
+#ifndef D3_PDL
+#define D3_PDL 1
+#endif
 
 namespace d3 {
 
@@ -84,6 +87,7 @@ djt_pass_kernel(const DjtPass p, const __grid_constant__ CUtensorMap zmap) {
     const int sig = g >> m;
     const int sg2 = sig & ((1 << c) - 1), sg1 = sig >> c;
     const int d10 = t1 * T1, d20 = t2 * T2;                 // stored output coords of the tile
+    if constexpr (FIRST && D3_PDL) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int D1abs = p.out_base + d10, D2abs = p.out_base + d20;
 
     Out *outp = reinterpret_cast<Out *>(p.out);
@@ -143,6 +147,8 @@ djt_pass_kernel(const DjtPass p, const __grid_constant__ CUtensorMap zmap) {
         }
     }
 
+    // programmatic dependent launch (DESIGN.md §5 item 8): wait for the previous pass's grid only now
+    if constexpr (!FIRST && D3_PDL) asm volatile("griddepcontrol.wait;" ::: "memory");
     // ---- stage the 2^K input planes' windows
     auto put = [&](int w, int i1, int i2, uint32_t bits) { sm[(w * WR + i1) * PJ + i2] = bits; };
     if constexpr (FIRST) {

@@ -240,6 +240,11 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
     const int tile = blockIdx.x, g = blockIdx.y, li = blockIdx.z;
     const int inst = p.inst0 + li;
     const int m = p.m, c = p.c;
+#ifndef D3_PDL
+#define D3_PDL 1
+#endif
+    // the next pass may be scheduled from now on (programmatic dependent launch, DESIGN.md §5 item 8)
+    if constexpr (!FINAL && D3_PDL) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int V2 = g & ((1 << m) - 1);
     const int V1 = (g >> m) & ((1 << m) - 1);
     const int sig = g >> (2 * m);
@@ -328,9 +333,6 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
 #ifdef D3_PROF_PASS
     const bool pp_on = tid == 0 && STAGE16 && FINAL;
     long long pp_t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#endif
-#ifndef D3_PDL
-#define D3_PDL 1
 #endif
     // programmatic dependent launch (DESIGN.md §5 item 8): a final pass may be scheduled while the
     // pass that writes its input finishes; zero tiles (above) need nothing from it, the rest wait

@@ -190,6 +190,19 @@ drt3d_status launch_djt_k(DjtPass prm, int ninst, cudaStream_t st) {
                 prm.zero_tma = 1;
         }
     }
+    if constexpr (!FIRST && D3_PDL) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(G::THREADS);
+        cfg.dynamicSmemBytes = G::SMEM;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, kern, prm, zmap) == cudaSuccess ? DRT3D_OK : DRT3D_ERR_CUDA;
+    }
     kern<<<grid, G::THREADS, G::SMEM, st>>>(prm, zmap);
     return DRT3D_OK;
 }
