@@ -56,7 +56,11 @@ def test_out_elems():
 
 def test_workspace_sizes():
     o = d3.make_opts()
-    assert d3.drt3d_planes_workspace_size(16, 0x1, o) == 0  # single pass, no intermediate
+    # N = 16: a few instances run two radix-4 passes (DESIGN.md §5 "Pass plan"), a large batch one
+    # stage-2 rows: N^2 x pitch round8(3N - base) u16, base = floor16(2N - 2 (2^2 - 1) - 7) = 16 -> 32
+    assert d3.drt3d_planes_workspace_size(16, 0x1, o) == 16 * 16 * 32 * 2
+    assert d3.drt3d_planes_workspace_size(16, 0xFFF, d3.make_opts(batch=64)) == 0   # single pass
+    assert d3.drt3d_planes_workspace_size(32, 0xFFF, o) == 0                  # u8 N = 32: on-chip kernel
     ws = d3.drt3d_planes_workspace_size(256, 0xFFF, o)
     # N=256, 12 dodecants in one chunk: 12 stage-4 buffers of N^2 rows x u16, pitch
     # round16(3N - base) with base = floor16(2N - 2 (2^4 - 1) - 7) = 464 -> 304
