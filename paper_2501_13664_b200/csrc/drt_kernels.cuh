@@ -192,11 +192,20 @@ __device__ __forceinline__ void drt_accumulate(const unsigned char *__restrict__
                 constexpr int r = decltype(r_)::value;
                 constexpr int o0 = TR ? (S - 1) - lk(K, a0, r) : lk(K, r, a0);
                 constexpr int o1 = TR ? (S - 1) - lk(K, a1, r) : lk(K, r, a1);
+// rows r with r % D3_FMA_MOD < D3_FMA_LT take their adds on the FMA pipe (round 2 re-sweep on the
+// cfg3 final pass: none 764 µs, 1/8 701, 1/4 689, 3/8 704, rows 0-1 mod 4 682, 5/8 687, 3/4 711,
+// even rows 677 -- and the backprojection 1.945 -> 1.768 ms); the transposed (adjoint) passes
+// have their own pair, D3_ADJ_FMA_MOD / LT
 #ifndef D3_FMA_MOD
-#define D3_FMA_MOD 4
+#define D3_FMA_MOD 2
 #define D3_FMA_LT 1
 #endif
-                constexpr bool fma = FMA16 < 0 ? (r % D3_FMA_MOD) < D3_FMA_LT : fma_row(r, FMA16);
+#ifndef D3_ADJ_FMA_MOD
+#define D3_ADJ_FMA_MOD 2
+#define D3_ADJ_FMA_LT 1
+#endif
+                constexpr bool fma = FMA16 < 0 ? (TR ? (r % D3_ADJ_FMA_MOD) < D3_ADJ_FMA_LT : (r % D3_FMA_MOD) < D3_FMA_LT)
+                                               : fma_row(r, FMA16);
 #ifndef D3_FADD2
 #define D3_FADD2 0                  // measured slower: cfg5 0.758 vs 0.741 ms, N=256 f32 2.03 vs 1.98 ms
 #endif
