@@ -105,7 +105,8 @@ struct Plan {
     int nset;               // 2: consecutive chunks use alternate buffer sets (cross-stream overlap)
     size_t ws_bytes;
     int nlaunch;
-    int small;              // 1: the on-chip N = 32 kernel (k_small.cu), one launch, no workspace
+    int small;              // 1: the on-chip N = 32 cluster kernel (k_small.cu), 2: the separable on-chip
+                            // N = 32 kernel (k_sep32.cu); one launch, no workspace
 };
 
 #ifndef D3_CHUNK_MB
@@ -271,6 +272,19 @@ drt3d_status make_plan(int transform, int N, uint32_t mask, const drt3d_opts &o,
     // default for u8 voxels at N = 32 (256 cubes x 12 dodecants: 1.00 vs 1.24 ms for the two
     // passes); measured slower for fp32 and int32 (cfg5: 1.06 vs 0.83 ms, DESIGN.md §5 "On-chip
     // N = 32"), which keep the two passes unless -DD3_SMALL32=1 (measurement builds; 2: never)
+#ifndef D3_SEP32
+#define D3_SEP32 1
+#endif
+    // the separable on-chip kernel (k_sep32.cu): two CTAs per instance, no exchange, no stage buffer;
+    // -DD3_SEP32=0 keeps the previous choices (measurement builds)
+    if (transform == 0 && N == 32 && o.layout == DRT3D_LAYOUT_STACKED && D3_SEP32) {
+        P.small = 2;
+        P.chunk = P.inst;
+        P.nset = 1;
+        P.ws_bytes = 0;
+        P.nlaunch = 1;
+        return DRT3D_OK;
+    }
     if (transform == 0 && N == 32 && o.layout == DRT3D_LAYOUT_STACKED && D3_SMALL32 != 2 &&
         (D3_SMALL32 == 1 || o.in_dtype == DRT3D_U8)) {
         P.small = 1;
@@ -478,7 +492,10 @@ drt3d_status run_drt(const void *cube, uint32_t mask, void *out, const drt3d_opt
         base.in = cube;
         base.out = out;
         drt3d_status s = DRT3D_OK;
-        drt3d_status ls = L.run(2, [&] { s = dispatch_drt_small32(o.in_dtype, base, P.inst, st); });
+        drt3d_status ls = L.run(2, [&] {
+            s = P.small == 2 ? dispatch_drt_sep32(o.in_dtype, base, P.inst, st)
+                             : dispatch_drt_small32(o.in_dtype, base, P.inst, st);
+        });
         if (s != DRT3D_OK) return s;
         if (o.launches) *o.launches = L.count;
         return ls;
