@@ -64,6 +64,20 @@ template <> struct Lane<float> {
     static __device__ __forceinline__ uint32_t bits(float v) { return __float_as_uint(v); }
 };
 
+// Two terms into an accumulator (the radix-2^K direct sums take rows two at a time).
+// Integer lanes: ~3/8 of the output rows take their two adds as IMAD x*one + acc
+// (FMA pipe, `one` a runtime 1) and the rest as one IADD3 (ALU pipe), so the
+// two integer-capable pipes share the work.
+template <class Acc>
+__device__ __forceinline__ Acc add2(Acc acc, uint32_t x, uint32_t y, uint32_t one, bool fma) {
+    if constexpr (std::is_same<Acc, uint32_t>::value) {
+        if (fma) return x * one + (y * one + acc);
+        return acc + x + y;
+    } else {
+        return acc + Lane<Acc>::get(x) + Lane<Acc>::get(y);
+    }
+}
+
 // element loads/stores converting between storage types and lane types
 template <class T> struct Elem;
 template <> struct Elem<uint8_t> {

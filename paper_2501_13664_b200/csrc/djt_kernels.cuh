@@ -212,52 +212,52 @@ djt_pass_kernel(const DjtPass p, const __grid_constant__ CUtensorMap zmap) {
         const int d1 = task % T1, rest = task / T1, rr = rest % NR, r1 = rest / NR;
         const int c0 = rr * (R / 4);
         Acc acc[S][R];
+        // l^K_{r1}(w) at run time (r1 is a per-thread value; only a row offset)
+        auto l1_of = [&](int w) {
+            int l1 = 0, s = r1, u = w;
 #pragma unroll
-        for (int r = 0; r < S; ++r)
-#pragma unroll
-            for (int j = 0; j < R; ++j) acc[r][j] = Acc(0);
-        static_for<0, S>([&](auto w_) {
-            constexpr int w = decltype(w_)::value;
-            constexpr int NC = (R + w + 3) / 4;
-            // l^K_{r1}(w) at run time (r1 is a per-thread value; only a row offset)
-            int l1 = 0;
-            {
-                int s = r1, u = w;
-#pragma unroll
-                for (int k = K; k >= 1; --k) {
-                    l1 += ((u >> (k - 1)) & 1) * ((s + 1) >> 1);
-                    s >>= 1;
-                    u &= (1 << (k - 1)) - 1;
-                }
+            for (int k = K; k >= 1; --k) {
+                l1 += ((u >> (k - 1)) & 1) * ((s + 1) >> 1);
+                s >>= 1;
+                u &= (1 << (k - 1)) - 1;
             }
-            const uint32_t *row = sm + (w * WR + d1 + l1) * PJ + c0 * 4;
-            uint32_t buf[NB * 4];
+            return l1;
+        };
+        auto load_plane = [&](int w, int nc, uint32_t *buf) {
+            const uint32_t *row = sm + (w * WR + d1 + l1_of(w)) * PJ + c0 * 4;
 #pragma unroll
-            for (int i = 0; i < NC; ++i) {
+            for (int i = 0; i < nc; ++i) {
                 const uint4 v = *reinterpret_cast<const uint4 *>(row + 4 * i);
                 buf[4 * i + 0] = v.x;
                 buf[4 * i + 1] = v.y;
                 buf[4 * i + 2] = v.z;
                 buf[4 * i + 3] = v.w;
             }
-            static_for<0, S>([&](auto r_) {
-                constexpr int r = decltype(r_)::value;
-                constexpr int off = lk(K, r, w);
-                if constexpr (std::is_same<Acc, float>::value && D3_FADD2 && R % 2 == 0) {
-                    // fp32: two outputs per instruction (sm_100 FADD2; off by default, drt_kernels.cuh)
+        };
+        if constexpr (S == 1) {
+            uint32_t buf[NB * 4];
+            load_plane(0, (R + 3) / 4, buf);
 #pragma unroll
-                    for (int j = 0; j < R; j += 2) {
-                        const float2 a = __fadd2_rn(make_float2(acc[r][j], acc[r][j + 1]),
-                                                    make_float2(__uint_as_float(buf[j + off]), __uint_as_float(buf[j + off + 1])));
-                        acc[r][j] = a.x;
-                        acc[r][j + 1] = a.y;
+            for (int j = 0; j < R; ++j) acc[0][j] = Lane<Acc>::get(buf[j]);
+        } else {
+            // planes two at a time: integer sums become 3-input adds; the first pair initialises
+            static_for<0, S / 2>([&](auto p_) {
+                constexpr int w0 = 2 * decltype(p_)::value, w1 = w0 + 1;
+                constexpr int NC0 = (R + w0 + 3) / 4, NC1 = (R + w1 + 3) / 4;
+                uint32_t b0[NC0 * 4], b1[NC1 * 4];
+                load_plane(w0, NC0, b0);
+                load_plane(w1, NC1, b1);
+                static_for<0, S>([&](auto r_) {
+                    constexpr int r = decltype(r_)::value;
+                    constexpr int o0 = lk(K, r, w0), o1 = lk(K, r, w1);
+#pragma unroll
+                    for (int j = 0; j < R; ++j) {
+                        if constexpr (w0 == 0) acc[r][j] = Lane<Acc>::get(b0[j + o0]) + Lane<Acc>::get(b1[j + o1]);
+                        else acc[r][j] = add2<Acc>(acc[r][j], b0[j + o0], b1[j + o1], 1u, false);
                     }
-                } else {
-#pragma unroll
-                    for (int j = 0; j < R; ++j) acc[r][j] = acc[r][j] + Lane<Acc>::get(buf[j + off]);
-                }
+                });
             });
-        });
+        }
         if constexpr (FINAL && sizeof(Out) == 4 && G::OUT_TMA) {
             if (p.zero_tma) {
                 // this warp's tasks = one r1: its S x T1 x T2 outputs go to the warp's image, then one

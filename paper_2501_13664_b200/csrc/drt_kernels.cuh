@@ -128,26 +128,14 @@ __device__ __forceinline__ int xswz(int c) { return c ^ ((c >> 3) & 1); }
 // acc[r][j] += sum_a row_a[j + l^K_r(a)] over the S staged rows slot(a) =
 // slot0 + a * sstep; the thread's run starts at chunk c0.  Rows are taken two
 // at a time so the integer sums become 3-input adds.
-// Integer lanes: ~3/8 of the output rows take their two adds as IMAD x*one + acc
-// (FMA pipe, `one` a runtime 1) and the rest as one IADD3 (ALU pipe), so the
-// two integer-capable pipes share the work.
-template <class Acc>
-__device__ __forceinline__ Acc add2(Acc acc, uint32_t x, uint32_t y, uint32_t one, bool fma) {
-    if constexpr (std::is_same<Acc, uint32_t>::value) {
-        if (fma) return x * one + (y * one + acc);
-        return acc + x + y;
-    } else {
-        return acc + Lane<Acc>::get(x) + Lane<Acc>::get(y);
-    }
-}
-
 // FMA16 of every 16 output rows take their adds on the FMA pipe (evenly spread over r).
 __host__ __device__ constexpr bool fma_row(int r, int fma16) { return ((r + 1) * fma16) / 16 > (r * fma16) / 16; }
 
 // FMA16 = -1: the measured default, rows with r % 4 < 1 (1/4 of the rows; swept 0 .. 3/8).
 // TR (transposed, the backprojection pass of adjoint_pass.cuh): output r, input a at offset
 // (S - 1) - l^K_a(r), i.e. acc[w][j] += row_r[j + H - l^K_r(w)].
-template <int K, int R, int SP, bool U16, class Acc, int FMA16 = -1, bool TR = false>
+// PB / PE: the row pairs (a0, a1) = (2p, 2p + 1), p in [PB, PE), taken (default: all).
+template <int K, int R, int SP, bool U16, class Acc, int FMA16 = -1, bool TR = false, int PB = 0, int PE = (1 << K) / 2>
 __device__ __forceinline__ void drt_accumulate(const unsigned char *__restrict__ sm, int slot0, int sstep, int c0,
                                                uint32_t one, Acc (&acc)[1 << K][R]) {
     constexpr int S = 1 << K;
@@ -181,7 +169,7 @@ __device__ __forceinline__ void drt_accumulate(const unsigned char *__restrict__
 #pragma unroll
         for (int j = 0; j < R; ++j) acc[0][j] = acc[0][j] + Lane<Acc>::get(b0[j]);
     } else {
-        static_for<0, S / 2>([&](auto p_) {
+        static_for<PB, PE>([&](auto p_) {
             constexpr int a0 = 2 * decltype(p_)::value, a1 = a0 + 1;
             // forward offsets l^K_r(a) <= a; transposed ones (S - 1) - l^K_a(r) reach S - 1
             constexpr int n0 = R + (TR ? S - 1 : a0), n1 = R + (TR ? S - 1 : a1);
@@ -241,6 +229,12 @@ __global__ void __maxnreg__((DrtGeom<K, R, T, !FIRST && sizeof(In) == 2>::MAXREG
 drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
     constexpr bool STAGE16 = !FIRST && sizeof(In) == 2;
     using G = DrtGeom<K, R, T, STAGE16>;
+#ifndef D3_SPLIT_STAGE
+#define D3_SPLIT_STAGE 0                 // measured: cfg3 final pass 0.703 vs 0.677 ms (the extra barrier costs more than the overlap)
+#endif
+    // u16 final passes: the staged rows arrive in two cp.async groups (rows w1 < S/2, then the rest);
+    // the x-step takes the first half's row pairs while the second half is still in flight
+    constexpr bool SPLIT = D3_SPLIT_STAGE && STAGE16 && FINAL && K >= 2;
     constexpr int S = G::S, SP = G::SP, BW = G::BW;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     unsigned char *sm = smem_raw;
@@ -570,18 +564,30 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
             const In *rb = inb + (rbase + ((long long)(V1 << K) << nc) + (V2 << K)) * p.in_pitch;
             unsigned char *dst = sm + sub * SP + 16 * (STAGE16 ? q : xswz(q));
             const int cq = cb + q;
-#pragma unroll 4
-            for (int slot = sub; slot < S * S; slot += SUBS, dst += SUBS * SP) {
+            auto copy = [&](int slot) {
                 const int w1 = slot >> K, w2 = slot & (S - 1);
                 const int cc = cq + ((sg1 * w1 + sg2 * w2) >> LOG_EPC);
                 const bool ok = (unsigned)cc < (unsigned)nchunk;
                 const uint32_t off = ((uint32_t)((w1 << nc) + w2) * (uint32_t)p.in_pitch + (uint32_t)(ok ? cc : 0) * EPC) *
                                      (uint32_t)sizeof(In);
                 cp_async16(dst, reinterpret_cast<const char *>(rb) + off, ok);
+            };
+            int slot = sub;
+            if constexpr (SPLIT) {
+                // rows w1 < S/2 (slots below S*S/2) in the first commit group, the rest in the second
+#pragma unroll 4
+                for (; slot < S * S / 2; slot += SUBS, dst += SUBS * SP) copy(slot);
+                asm volatile("cp.async.commit_group;" ::: "memory");
             }
+#pragma unroll 4
+            for (; slot < S * S; slot += SUBS, dst += SUBS * SP) copy(slot);
         }
         PP_MARK(1);
-        cp_async_wait_all();
+        if constexpr (SPLIT) {
+            asm volatile("cp.async.commit_group;\ncp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            cp_async_wait_all();
+        }
     }
     __syncthreads();
     PP_MARK(2);
@@ -619,7 +625,15 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
     };
     if constexpr (STAGE16) {
         // x-step reads the u16 staged rows, y-step the 32-bit X rows
-        if (tid < G::XT) {
+        if constexpr (SPLIT) {
+            if (tid < G::XT) {
+                zero_acc();
+                drt_accumulate<K, R, SP, true, Acc, -1, false, 0, S / 4>(sm, xb, S, xr * (R / 8), p.one, acc);
+            }
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncthreads();                                 // every thread's second-half rows have landed
+            if (tid < G::XT) drt_accumulate<K, R, SP, true, Acc, -1, false, S / 4, S / 2>(sm, xb, S, xr * (R / 8), p.one, acc);
+        } else if (tid < G::XT) {
             zero_acc();
             drt_accumulate<K, R, SP, true, Acc>(sm, xb, S, xr * (R / 8), p.one, acc);
         }

@@ -34,6 +34,11 @@ namespace d3 {
 namespace sep32 {
 
 constexpr int N = 32, CL = 4, THREADS = 256, R = 8;
+// -DD3_SEP_ABL=mask (ablation builds, wrong results): 1 no Y2 stores, 2 no remote Q stores,
+// 4 no y part, 8 no x part
+#ifndef D3_SEP_ABL
+#define D3_SEP_ABL 0
+#endif
 
 // -DD3_PROF_SEP32: per-phase clock accounting (lane 0 of warps 0 and 7) into d3_sep_prof[]
 #ifdef D3_PROF_SEP32
@@ -234,27 +239,41 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(THREADS, 2) drt_sep
         const int y = tid & 31, run = tid >> 5;
         Acc acc[8][R];
         auto rc = [&](int a, int c) -> const unsigned char * { return slab_chunk(a * 32 + y, c); };
-        radix8<8, 0, R, Acc>(rc, 2 * run - 2, p.one, acc);
+        if (!(D3_SEP_ABL & 8)) radix8<8, 0, R, Acc>(rc, 2 * run - 2, p.one, acc);
         // every CTA of the cluster has started (arrive at entry) before any remote store
         asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
 #pragma unroll
         for (int s = 0; s < 8; ++s) {
-            unsigned char *q = cluster.map_shared_rank(smQ, s >> 1) + (((s & 1) * 4 + k) * 32 + y) * QP * 16;
+            unsigned char *q = cluster.map_shared_rank(smQ, (D3_SEP_ABL & 2) ? k : (s >> 1)) + (((s & 1) * 4 + k) * 32 + y) * QP * 16;
             put_run<Acc>(q, 2 * run, acc[s]);
         }
     } else {
-        // one bulk copy (TMA engine) of the zero region per output row prefix
-        const uint32_t zsrc = static_cast<uint32_t>(__cvta_generic_to_shared(zero));
-        for (int row = tid - 5 * 32; row < 8 * 32; row += THREADS - 5 * 32) {     // row = s1l * 32 + s2
-            const int s1 = 8 * k + (row >> 5), s2 = row & 31;
-            const int lim = 2 * N - s1 - (4 * (s2 >> 2) + 3), nz = lim > 0 ? lim / 12 : 0;
-            if (nz > 0)
-                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
-                                 outp + ((long long)s1 * N + s2) * (3 * N)),
-                             "r"(zsrc), "r"(48 * nz)
-                             : "memory");
+#ifndef D3_SEP_ZERO
+#define D3_SEP_ZERO 0        // 0: one bulk copy (TMA) per row prefix here, overlapping X1 (default); measured:
+                             // 1 16-byte stores here (f32 0.760 ms vs 0.713), 3 Y2 stores whole rows, zeros
+                             // included (0.729); 2 none (ablation)
+#endif
+        if constexpr (D3_SEP_ZERO == 0) {
+            // one bulk copy (TMA engine) of the zero region per output row prefix
+            const uint32_t zsrc = static_cast<uint32_t>(__cvta_generic_to_shared(zero));
+            for (int row = tid - 5 * 32; row < 8 * 32; row += THREADS - 5 * 32) {     // row = s1l * 32 + s2
+                const int s1 = 8 * k + (row >> 5), s2 = row & 31;
+                const int lim = 2 * N - s1 - (4 * (s2 >> 2) + 3), nz = lim > 0 ? lim / 12 : 0;
+                if (nz > 0)
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                                     outp + ((long long)s1 * N + s2) * (3 * N)),
+                                 "r"(zsrc), "r"(48 * nz)
+                                 : "memory");
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        } else if constexpr (D3_SEP_ZERO == 1) {
+            for (int row = tid - 5 * 32; row < 8 * 32; row += THREADS - 5 * 32) {
+                const int s1 = 8 * k + (row >> 5), s2 = row & 31;
+                const int lim = 2 * N - s1 - (4 * (s2 >> 2) + 3), nz = lim > 0 ? lim / 12 : 0;
+                Acc *d = outp + ((long long)s1 * N + s2) * (3 * N);
+                for (int r = 0; r < 3 * nz; ++r) st_cs_v4(d + 4 * r, 0u, 0u, 0u, 0u);
+            }
         }
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
     }
     // every Q row has arrived (release / acquire at cluster scope)
@@ -265,7 +284,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(THREADS, 2) drt_sep
 
     // ---- X2: task (sl, run, y), lanes on y; P(s1 = 4 sig1 + rho1, y)[p = 8 run + j], sig1 = 2k + sl,
     // p = t + 32 in [0, 64): Q at q = p - 24 + sig1 V1 + l^2_rho1(V1) (chunks 2 run - 6 + .., valid 0..9)
-    for (int t = tid; t < 2 * 8 * 32; t += THREADS) {
+    for (int t = tid; t < ((D3_SEP_ABL & 8) ? 0 : 2 * 8 * 32); t += THREADS) {
         const int y = t & 31, run = (t >> 5) & 7, sl = t >> 8, sig1 = 2 * k + sl;
         Acc acc[4][R];
         if (8 * run + 8 > 32 - (4 * sig1 + 3)) {            // else below the support of all 4 slopes
@@ -296,7 +315,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(THREADS, 2) drt_sep
     // t >= -(s1 + sig2): u = t + 40 in [8, 72) (16 runs of 4) for s1 < 24, [0, 72) (18 runs) above.
     const int ulo = k == 3 ? 0 : 2, nrun1 = 18 - ulo;
 #pragma unroll 1
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < ((D3_SEP_ABL & 4) ? 0 : 2); ++b) {
         // Y1: task (sb, V2, run), lanes on run; U(sb; sig2, V2)[u = 4 run + j]: P(s1, 8 V2 + w2) at
         // p = u - 8 + l^3_sig2(w2) (chunks run - 2 + .., valid 0..15)
         for (int t = tid; t < 4 * 4 * nrun1; t += THREADS) {
@@ -323,14 +342,27 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(THREADS, 2) drt_sep
             constexpr int R2 = 12;
             const int sig2 = tid >> 5, sb = (tid >> 3) & 3, run = tid & 7;
             const int s1 = 8 * k + 4 * b + sb;
-            if (12 * run + 12 > 2 * N - s1 - (4 * sig2 + 3)) {      // else zeros, written above
-                Acc acc[4][R2];
+            bool skip = false;
+            Acc acc[4][R2];
+            if (12 * run + 12 > 2 * N - s1 - (4 * sig2 + 3)) {
                 auto rc = [&](int V2, int c) -> const unsigned char * {
                     return (unsigned)(c - ulo) < (unsigned)(UCH - ulo) ? smQ + (((sb * 8 + sig2) * 4 + V2) * UP + c) * 16
                                                                        : zero;
                 };
                 with_const8<0>(sig2, [&](auto S_) { radix4<decltype(S_)::value, R2, Acc>(rc, 3 * run - 6, p.one, acc); });
-                Acc *orow = outp + ((long long)s1 * N + 4 * sig2) * (3 * N) + R2 * run;
+            } else {
+                // wholly below the support of the 4 rows: zeros (written by the block's own stores unless the
+                // X1-phase zero writer did, D3_SEP_ZERO < 3)
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+#pragma unroll
+                    for (int j = 0; j < R2; ++j) acc[q][j] = Acc(0);
+                if (D3_SEP_ZERO < 3) skip = true;
+            }
+            Acc *orow = outp + ((long long)s1 * N + 4 * sig2) * (3 * N) + R2 * run;
+            if (D3_SEP_ABL & 1) {
+                if (Lane<Acc>::bits(acc[0][0]) == 0x7f7f7f7fu) orow[0] = acc[3][11];   // keep the sums live
+            } else if (!skip) {
 #pragma unroll
                 for (int rho = 0; rho < 4; ++rho)
 #pragma unroll
@@ -345,7 +377,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(THREADS, 2) drt_sep
 #endif
     }
     // the zero region must outlive the bulk zero stores' shared-memory reads
-    if (tid >= 5 * 32) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    if (D3_SEP_ZERO == 0 && tid >= 5 * 32) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 #ifdef D3_PROF_SEP32
     sp_t[7] = clock64();
     if ((tid & 31) == 0 && (tid == 0 || tid == 224)) {
