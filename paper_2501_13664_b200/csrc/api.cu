@@ -268,15 +268,15 @@ drt3d_status make_plan(int transform, int N, uint32_t mask, const drt3d_opts &o,
 #ifndef D3_SMALL32
 #define D3_SMALL32 0
 #endif
-    // every stage on chip in one 8-CTA cluster per instance (k_small.cu), no stage buffers: the
-    // default for u8 voxels at N = 32 (256 cubes x 12 dodecants: 1.00 vs 1.24 ms for the two
-    // passes); measured slower for fp32 and int32 (cfg5: 1.06 vs 0.83 ms, DESIGN.md §5 "On-chip
-    // N = 32"), which keep the two passes unless -DD3_SMALL32=1 (measurement builds; 2: never)
+    // round 1: every stage on chip in one 8-CTA cluster per instance (k_small.cu) for u8 voxels at
+    // N = 32 (0.990 ms this round), the two passes for fp32 / int32 (0.739 / 0.731 ms); reached only
+    // with -DD3_SEP32=0 (-DD3_SMALL32=1: k_small for every dtype; 2: never)
 #ifndef D3_SEP32
 #define D3_SEP32 1
 #endif
-    // the separable on-chip kernel (k_sep32.cu): two CTAs per instance, no exchange, no stage buffer;
-    // -DD3_SEP32=0 keeps the previous choices (measurement builds)
+    // the separable on-chip kernel (k_sep32.cu): one 4-CTA cluster per instance, no stage buffer; the
+    // default at N = 32 for every dtype (256 cubes x 12 dodecants: u8 0.642 ms, i32 0.686, f32 0.713;
+    // DESIGN.md §5e).  -DD3_SEP32=0 restores the round-1 choices below (measurement builds)
     if (transform == 0 && N == 32 && o.layout == DRT3D_LAYOUT_STACKED && D3_SEP32) {
         P.small = 2;
         P.chunk = P.inst;
