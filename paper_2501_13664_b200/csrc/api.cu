@@ -106,7 +106,8 @@ struct Plan {
     size_t ws_bytes;
     int nlaunch;
     int small;              // 1: the on-chip N = 32 cluster kernel (k_small.cu), 2: the separable on-chip
-                            // N = 32 kernel (k_sep32.cu); one launch, no workspace
+                            // N = 32 kernel (k_sep32.cu), 3: the one-CTA N = 16 kernel (k_sep16.cu);
+                            // one launch, no workspace
 };
 
 #ifndef D3_CHUNK_MB
@@ -277,6 +278,19 @@ drt3d_status make_plan(int transform, int N, uint32_t mask, const drt3d_opts &o,
     // the separable on-chip kernel (k_sep32.cu): one 4-CTA cluster per instance, no stage buffer; the
     // default at N = 32 for every dtype (256 cubes x 12 dodecants: u8 0.642 ms, i32 0.686, f32 0.713;
     // DESIGN.md §5e).  -DD3_SEP32=0 restores the round-1 choices below (measurement builds)
+#ifndef D3_SEP16
+#define D3_SEP16 1
+#endif
+    // N = 16: every stage of an instance in one CTA (k_sep16.cu), one launch, no stage buffer;
+    // -DD3_SEP16=0 keeps the pass kernels (measurement builds)
+    if (transform == 0 && N == 16 && o.layout == DRT3D_LAYOUT_STACKED && D3_SEP16) {
+        P.small = 3;
+        P.chunk = P.inst;
+        P.nset = 1;
+        P.ws_bytes = 0;
+        P.nlaunch = 1;
+        return DRT3D_OK;
+    }
     if (transform == 0 && N == 32 && o.layout == DRT3D_LAYOUT_STACKED && D3_SEP32) {
         P.small = 2;
         P.chunk = P.inst;
@@ -493,8 +507,9 @@ drt3d_status run_drt(const void *cube, uint32_t mask, void *out, const drt3d_opt
         base.out = out;
         drt3d_status s = DRT3D_OK;
         drt3d_status ls = L.run(2, [&] {
-            s = P.small == 2 ? dispatch_drt_sep32(o.in_dtype, base, P.inst, st)
-                             : dispatch_drt_small32(o.in_dtype, base, P.inst, st);
+            s = P.small == 3   ? dispatch_drt_sep16(o.in_dtype, base, P.inst, st)
+                : P.small == 2 ? dispatch_drt_sep32(o.in_dtype, base, P.inst, st)
+                               : dispatch_drt_small32(o.in_dtype, base, P.inst, st);
         });
         if (s != DRT3D_OK) return s;
         if (o.launches) *o.launches = L.count;

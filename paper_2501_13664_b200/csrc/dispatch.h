@@ -19,4 +19,6 @@ D3_DECL(dispatch_djt_f32, DjtPass)
 drt3d_status dispatch_drt_small32(int in_dtype, const DrtPass &prm, int ninst, cudaStream_t st);
 // the separable on-chip N = 32 DRT (k_sep32.cu): two independent CTAs per instance
 drt3d_status dispatch_drt_sep32(int in_dtype, const DrtPass &prm, int ninst, cudaStream_t st);
+// the one-CTA N = 16 DRT (k_sep16.cu)
+drt3d_status dispatch_drt_sep16(int in_dtype, const DrtPass &prm, int ninst, cudaStream_t st);
 }  // namespace d3

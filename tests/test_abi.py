@@ -56,10 +56,13 @@ def test_out_elems():
 
 def test_workspace_sizes():
     o = d3.make_opts()
-    # N = 16: a few instances run two radix-4 passes (DESIGN.md §5 "Pass plan"), a large batch one
-    # stage-2 rows: N^2 x pitch round8(3N - base) u16, base = floor16(2N - 2 (2^2 - 1) - 7) = 16 -> 32
-    assert d3.drt3d_planes_workspace_size(16, 0x1, o) == 16 * 16 * 32 * 2
-    assert d3.drt3d_planes_workspace_size(16, 0xFFF, d3.make_opts(batch=64)) == 0   # single pass
+    # N = 16 stacked: every stage of an instance in one CTA (k_sep16.cu), no workspace
+    assert d3.drt3d_planes_workspace_size(16, 0x1, o) == 0
+    assert d3.drt3d_planes_workspace_size(16, 0xFFF, d3.make_opts(batch=64)) == 0
+    # N = 16 mosaic: the pass kernels; 12 instances run two radix-4 passes (DESIGN.md §5 "Pass plan"):
+    # stage-2 rows N^2 x pitch round8(3N - base) u16, base = floor16(2N - 2 (2^2 - 1) - 7) = 16 -> 32
+    om = d3.make_opts(layout=d3.DRT3D_LAYOUT_MOSAIC)
+    assert d3.drt3d_planes_workspace_size(16, 0xFFF, om) == 12 * 16 * 16 * 32 * 2
     assert d3.drt3d_planes_workspace_size(32, 0xFFF, o) == 0                  # u8 N = 32: on-chip kernel
     ws = d3.drt3d_planes_workspace_size(256, 0xFFF, o)
     # N=256, 12 dodecants in one chunk: 12 stage-4 buffers of N^2 rows x u16, pitch

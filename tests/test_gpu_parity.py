@@ -176,6 +176,22 @@ def test_drt_float_small_all_tables():
         assert np.all(np.abs(got[b] - ref) <= 1e-5 * refabs)
 
 
+def test_drt_n16_one_cta_batched():
+    """N = 16 runs every stage of an instance in one CTA (k_sep16.cu): one cube x 12 dodecants and
+    16 cubes x 12 (more instances than SMs); int32 bit-exact, fp32 within the T1 gate."""
+    for batch in (1, 16):
+        cube = synth.uniform_cube(16, 70 + batch, np.int32, -1000, 1000, batch=batch)
+        got = _planes(cube, 0xFFF)
+        for b in range(batch):
+            assert np.array_equal(got[b].astype(np.int64), oracle.drt_planes(cube[b], 0xFFF))
+        cubef = synth.normal_cube(16, 80 + batch, batch=batch)
+        gotf = _planes(cubef, 0xFFF)
+        for b in range(batch):
+            ref = oracle.drt_planes(cubef[b].astype(np.float64), 0xFFF)
+            refabs = oracle.drt_planes(np.abs(cubef[b]).astype(np.float64), 0xFFF)
+            assert np.all(np.abs(gotf[b] - ref) <= 1e-5 * refabs)
+
+
 def test_drt_mosaic_layout():
     # N = 128: the u16 SWAR first pass and the K = 3 final pass's mosaic stores
     for N in (4, 32, 128):
