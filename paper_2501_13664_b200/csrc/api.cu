@@ -105,7 +105,7 @@ struct Plan {
     int nset;               // 2: consecutive chunks use alternate buffer sets (cross-stream overlap)
     size_t ws_bytes;
     int nlaunch;
-    int small;              // 1: the on-chip N = 32 cluster kernel (k_small.cu), 2: the separable on-chip
+    int small;              // 2: the separable on-chip
                             // N = 32 kernel (k_sep32.cu), 3: the one-CTA N = 16 kernel (k_sep16.cu);
                             // one launch, no workspace
 };
@@ -266,18 +266,6 @@ drt3d_status make_plan(int transform, int N, uint32_t mask, const drt3d_opts &o,
         }
     }
     P.base[0] = transform == 0 ? 2 * N : N;
-#ifndef D3_SMALL32
-#define D3_SMALL32 0
-#endif
-    // round 1: every stage on chip in one 8-CTA cluster per instance (k_small.cu) for u8 voxels at
-    // N = 32 (0.990 ms this round), the two passes for fp32 / int32 (0.739 / 0.731 ms); reached only
-    // with -DD3_SEP32=0 (-DD3_SMALL32=1: k_small for every dtype; 2: never)
-#ifndef D3_SEP32
-#define D3_SEP32 1
-#endif
-    // the separable on-chip kernel (k_sep32.cu): one 4-CTA cluster per instance, no stage buffer; the
-    // default at N = 32 for every dtype (256 cubes x 12 dodecants: u8 0.642 ms, i32 0.686, f32 0.713;
-    // DESIGN.md §5e).  -DD3_SEP32=0 restores the round-1 choices below (measurement builds)
 #ifndef D3_SEP16
 #define D3_SEP16 1
 #endif
@@ -293,15 +281,6 @@ drt3d_status make_plan(int transform, int N, uint32_t mask, const drt3d_opts &o,
     }
     if (transform == 0 && N == 32 && o.layout == DRT3D_LAYOUT_STACKED && D3_SEP32) {
         P.small = 2;
-        P.chunk = P.inst;
-        P.nset = 1;
-        P.ws_bytes = 0;
-        P.nlaunch = 1;
-        return DRT3D_OK;
-    }
-    if (transform == 0 && N == 32 && o.layout == DRT3D_LAYOUT_STACKED && D3_SMALL32 != 2 &&
-        (D3_SMALL32 == 1 || o.in_dtype == DRT3D_U8)) {
-        P.small = 1;
         P.chunk = P.inst;
         P.nset = 1;
         P.ws_bytes = 0;
@@ -507,9 +486,8 @@ drt3d_status run_drt(const void *cube, uint32_t mask, void *out, const drt3d_opt
         base.out = out;
         drt3d_status s = DRT3D_OK;
         drt3d_status ls = L.run(2, [&] {
-            s = P.small == 3   ? dispatch_drt_sep16(o.in_dtype, base, P.inst, st)
-                : P.small == 2 ? dispatch_drt_sep32(o.in_dtype, base, P.inst, st)
-                               : dispatch_drt_small32(o.in_dtype, base, P.inst, st);
+            s = P.small == 3 ? dispatch_drt_sep16(o.in_dtype, base, P.inst, st)
+                             : dispatch_drt_sep32(o.in_dtype, base, P.inst, st);
         });
         if (s != DRT3D_OK) return s;
         if (o.launches) *o.launches = L.count;

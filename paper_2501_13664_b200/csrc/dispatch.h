@@ -15,8 +15,6 @@ D3_DECL(dispatch_djt_u8, DjtPass)
 D3_DECL(dispatch_djt_i32, DjtPass)
 D3_DECL(dispatch_djt_f32, DjtPass)
 #undef D3_DECL
-// the on-chip N = 32 DRT (k_small.cu): every stage of each instance in one 8-CTA cluster
-drt3d_status dispatch_drt_small32(int in_dtype, const DrtPass &prm, int ninst, cudaStream_t st);
 // the separable on-chip N = 32 DRT (k_sep32.cu): two independent CTAs per instance
 drt3d_status dispatch_drt_sep32(int in_dtype, const DrtPass &prm, int ninst, cudaStream_t st);
 // the one-CTA N = 16 DRT (k_sep16.cu)
