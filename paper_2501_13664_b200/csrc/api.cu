@@ -279,6 +279,13 @@ drt3d_status make_plan(int transform, int N, uint32_t mask, const drt3d_opts &o,
         P.nlaunch = 1;
         return DRT3D_OK;
     }
+#ifndef D3_SEP32
+#define D3_SEP32 1
+#endif
+    // N = 32: the separable on-chip kernel (k_sep32.cu), one 4-CTA cluster per instance, no stage
+    // buffer; default for every dtype (256 cubes x 12 dodecants: u8 0.642 ms, i32 0.686, f32 0.713,
+    // against 0.990 / 0.731 / 0.739 for round 1's kernels).  -DD3_SEP32=0 keeps the
+    // pass kernels (measurement builds)
     if (transform == 0 && N == 32 && o.layout == DRT3D_LAYOUT_STACKED && D3_SEP32) {
         P.small = 2;
         P.chunk = P.inst;
