@@ -509,7 +509,9 @@ drt_first_swar_kernel(const DrtPass p, const __grid_constant__ CUtensorMap zmap)
         const int gs2 = g & (S - 1), gs1 = g >> K;
         const int nz = (2 * N - ((gs1 << K) + S - 1) - ((gs2 << K) + S - 1)) / p.zf_T;
         if ((int)blockIdx.x < nz) {
-            static_assert(K != 4 || G::SMEM >= S * S * D3_FINAL16_T * 4, "a zero tile image fits the shared memory");
+            if constexpr (K == 4 && G::SMEM < S * S * D3_FINAL16_T * 4) {
+                __trap();                                     // a zero tile image must fit (host checks zf_T)
+            }
             __syncthreads();                                  // every copy-out read is done
             for (int i = tid; i < S * S * p.zf_T / 4; i += blockDim.x)
                 reinterpret_cast<uint4 *>(sm)[i] = make_uint4(0u, 0u, 0u, 0u);

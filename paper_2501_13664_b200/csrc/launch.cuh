@@ -9,6 +9,8 @@
 
 namespace d3 {
 
+template <int A, int B> struct IntPair { static constexpr int first = A, second = B; };
+
 // ---- DRT kernel selection
 template <int K> struct DrtTile;
 template <> struct DrtTile<1> { static constexpr int R = 8, T = 128; };
@@ -68,21 +70,38 @@ drt3d_status launch_drt_k(const DrtPass &prm_in, int ninst, cudaStream_t st) {
 #define SWAR_R 8
 #endif
         constexpr int RS = SWAR_R;
-        using SG = SwarGeom<K, RS, T>;
-        auto kern = drt_first_swar_kernel<K, RS, T>;
-        static std::atomic<uint32_t> smem_done{0};
-        if (!set_smem_once(kern, SG::SMEM, smem_done)) return DRT3D_ERR_CUDA;
-        const int ntiles = (prm.out_width + 8 + T - 1) / T;
-        dim3 grid(ntiles, (unsigned)(1LL << (2 * prm.m)), ninst);
-        // the final pass's zero tiles (api.cu, DESIGN.md §5 item 6): map of the final output
-        CUtensorMap zmap;
-        std::memset(&zmap, 0, sizeof(zmap));
-        DrtPass q = prm;
-        if (q.zf_T > 0 && !(K == 4 && q.zf_T == D3_FINAL16_T &&
-                            make_out_map(&zmap, q.zf_out, q.N, q.inst_total, q.zf_T, 1 << K, 1 << K)))
-            return DRT3D_ERR_UNSUPPORTED;
-        kern<<<grid, SG::THREADS, SG::SMEM, st>>>(q, zmap);
-        return DRT3D_OK;
+        // few tiles (under D3_SWAR_SMALL_CTAS CTAs at T = 64, about one per SM): half-width tiles
+        // (T = 32, R = 4), twice the CTAs on the latency-bound per-tile chain.  Measured at N = 64:
+        // one dodecant (32 CTAs) 0.0154 -> 0.0133 ms; 12 dodecants (384 CTAs) 0.0317 -> 0.0338 (kept
+        // at T = 64 by the threshold)
+#ifndef D3_SWAR_SMALL_CTAS
+#define D3_SWAR_SMALL_CTAS 160
+#endif
+        const long long groups = 1LL << (2 * prm.m);
+        const bool half = K == 4 && T == 64 && prm.zf_T == 0 &&
+                          (long long)((prm.out_width + 8 + T - 1) / T) * groups * ninst < D3_SWAR_SMALL_CTAS;
+        auto go = [&](auto geo) -> drt3d_status {
+            constexpr int RR = decltype(geo)::first, TT = decltype(geo)::second;
+            using SG = SwarGeom<K, RR, TT>;
+            auto kern = drt_first_swar_kernel<K, RR, TT>;
+            static std::atomic<uint32_t> smem_done{0};
+            if (!set_smem_once(kern, SG::SMEM, smem_done)) return DRT3D_ERR_CUDA;
+            const int ntiles = (prm.out_width + 8 + TT - 1) / TT;
+            dim3 grid(ntiles, (unsigned)groups, ninst);
+            // the final pass's zero tiles (api.cu, DESIGN.md §5 item 6): map of the final output
+            CUtensorMap zmap;
+            std::memset(&zmap, 0, sizeof(zmap));
+            DrtPass q = prm;
+            if (q.zf_T > 0 && !(K == 4 && q.zf_T == D3_FINAL16_T && SG::SMEM >= (1 << (2 * K)) * D3_FINAL16_T * 4 &&
+                                make_out_map(&zmap, q.zf_out, q.N, q.inst_total, q.zf_T, 1 << K, 1 << K)))
+                return DRT3D_ERR_UNSUPPORTED;
+            kern<<<grid, SG::THREADS, SG::SMEM, st>>>(q, zmap);
+            return DRT3D_OK;
+        };
+        if constexpr (K == 4 && T == 64) {
+            if (half) return go(IntPair<4, 32>{});
+        }
+        return go(IntPair<RS, T>{});
     }
     using G = DrtGeom<K, R, T, !FIRST && sizeof(In) == 2>;
     auto kern = drt_pass_kernel<K, R, T, In, Acc, Out, FIRST, FINAL>;
