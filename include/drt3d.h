@@ -100,7 +100,10 @@ drt3d_status drt3d_orientation_table(int table, int transform, int8_t rows[36]);
  * repaired rows (-1,-2,3), (-2,1,3), (1,2,3), (2,-1,3) of DESIGN.md reading
  * R13: with them, and only them, the boundary planes neighbouring dodecants
  * share lie on facing block edges ("rotated so that all of them fit
- * accurately", fig:shapeOutput; HEMISPHERE table).        */
+ * accurately", fig:shapeOutput; HEMISPHERE table).
+ * Workspace: drt3d_planes_workspace_size() bytes (device, 256-byte aligned);
+ * 0 for N = 16 and N = 32 in the STACKED layout (every stage on chip), where
+ * workspace may be NULL.                                                      */
 size_t drt3d_planes_out_elems(int N, uint32_t dodecant_mask, const drt3d_opts *opts);
 drt3d_status drt3d_planes_workspace_size(int N, uint32_t dodecant_mask, const drt3d_opts *opts,
                                          size_t *bytes);
