@@ -227,13 +227,24 @@ def test_drt_deterministic():
     assert np.array_equal(a, b)
 
 
-def test_drt_int32_wraps_mod_2_32():
-    # int32 output = exact sum mod 2^32 (include/drt3d.h)
-    N = 8
+@pytest.mark.parametrize("N", [8, 16, 32, 64])
+def test_drt_int32_wraps_mod_2_32(N):
+    # int32 output = exact sum mod 2^32 (include/drt3d.h); N = 16 / 32 run the on-chip kernels
+    # (k_sep16 / k_sep32, whose partial sums P, Q, U wrap too), 8 and 64 the pass kernels
     cube = np.full((N, N, N), 2 ** 30, np.int32)
-    got = _planes(cube, 0x001)
-    ref = oracle.drt_planes(cube.astype(np.int64), 0x001)
+    cube[::3, 1::2, ::5] = -(2 ** 31) + 7
+    got = _planes(cube, 0xFFF)
+    ref = oracle.drt_planes(cube.astype(np.int64), 0xFFF)
     assert np.array_equal(got.astype(np.int64), ((ref + 2 ** 31) % 2 ** 32) - 2 ** 31)
+
+
+@pytest.mark.parametrize("N", [16, 32])
+def test_drt_saturated_u8_on_chip(N):
+    # all-255 u8 cubes through the on-chip kernels: the largest sums (255 N^2), all 12 dodecants
+    cube = np.full((2, N, N, N), 255, np.uint8)
+    got = _planes(cube, 0xFFF)
+    ref = oracle.drt_planes(cube[0], 0xFFF)
+    assert np.array_equal(got[0].astype(np.int64), ref) and np.array_equal(got[1], got[0])
 
 
 # ------------------------------------------------------------ 3D DJT
