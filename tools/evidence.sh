@@ -13,6 +13,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:d
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/ev_ncul_$TAG.log 2>&1; echo ncul=$? >> $S
 timeout 900 ncu --set full --import-source on --clock-control none --cache-control none -k regex:drt -s 6 -c 2 -o gpurun_out/ev_prof_$TAG -f \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/ev_ncu_$TAG.log 2>&1; echo ncu=$? >> $S
+/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -shared -Xcompiler -fPIC tools/write_probe.cu -o tools/libwrite_probe.so > gpurun_out/ev_hbm_build_$TAG.log 2>&1
 timeout 300 python tools/hbm_write_probe.py > gpurun_out/ev_hbm_$TAG.log 2>&1; echo hbm=$? >> $S
 timeout 600 python tools/bench_configs.py > gpurun_out/ev_configs_$TAG.log 2>&1; echo configs=$? >> $S
 cat $S
