@@ -123,7 +123,9 @@ drt3d_status launch_drt_k(const DrtPass &prm_in, int ninst, cudaStream_t st) {
         constexpr int S = 1 << K;
         if (!no_tma && prm.layout == 0 && prm.m == 0 && prm.out_width % T == 0 && S * S * T * 4 <= G::SMEM &&
             make_out_map(&omap, prm.out, prm.N, prm.inst_total, T, S,
-                         drt_warp_store<K, R, T, !FIRST && sizeof(In) == 2, FINAL>() ? 4 : S))
+                         drt_warp_store<K, R, T, !FIRST && sizeof(In) == 2, FINAL>()    ? 4
+                         : drt_hybrid_store<K, R, T, !FIRST && sizeof(In) == 2, FINAL>() ? S / 2
+                                                                                        : S))
             prm.tma_store = 1;
     }
     if constexpr (!FIRST && D3_PDL) {
