@@ -466,7 +466,9 @@ struct JoinGuard {
 // Each instance has its own stage buffer slice inside the chunk, so groups never wait on each
 // other's buffers; consecutive chunks of large batches alternate between two buffer sets.
 drt3d_status run_drt(const void *cube, uint32_t mask, void *out, const drt3d_opts &o, const Plan &P, void *ws,
-                     cudaStream_t st) {
+                     cudaStream_t st, bool reduce_sub = false) {
+    if (reduce_sub && (P.small || o.layout != DRT3D_LAYOUT_STACKED || o.out_dtype != DRT3D_F32))
+        return DRT3D_ERR_UNSUPPORTED;
     const int8_t(*rows)[3] = table_rows(o.table, 0);
     DrtPass base{};
     base.N = P.N;
@@ -553,6 +555,7 @@ drt3d_status run_drt(const void *cube, uint32_t mask, void *out, const drt3d_opt
                     prm.zf_inst_stride = final_inst;
                 }
                 if (zfirst && fin) prm.zeros_by_first = 1;
+                prm.reduce_sub = (reduce_sub && fin) ? 1 : 0;
                 drt3d_status s = DRT3D_OK;
                 drt3d_status ls = L.run_on(ps, first ? 0 : (fin ? 2 : 1), [&] {
                     s = dispatch_drt(o.in_dtype, P.ks[p], P.stor[p], P.stor[p + 1], first, fin, prm, gn, ps);
@@ -844,3 +847,25 @@ drt3d_status djt3d_lines_host(const void *host_cube, int N, uint32_t mask, void 
 }
 
 }  // extern "C"
+
+namespace d3 {
+// Internal entry (C++ linkage, not part of the C ABI): r <- r - A f for an fp32 cube, stacked
+// layout, enqueued on `stream`.  The final pass adds -A f into r with a TMA reduce-add per output
+// tile (its all-zero tiles add nothing), so the residual update of the inverse (invert.cu) needs no
+// separate elementwise pass over A f.  DRT3D_ERR_UNSUPPORTED, with nothing enqueued, for plans
+// without that final pass (N < 64: the on-chip kernels, the tiny single passes).
+drt3d_status planes_residual(const void *cube, int N, uint32_t mask, float *r, const drt3d_opts *opts,
+                             void *workspace, size_t workspace_bytes, void *stream) {
+    drt3d_opts tmp;
+    const drt3d_opts &o = opts_or_default(opts, tmp);
+    if (o.in_dtype != DRT3D_F32 || o.out_dtype != DRT3D_F32 || o.layout != DRT3D_LAYOUT_STACKED || N < 64)
+        return DRT3D_ERR_UNSUPPORTED;
+    Plan P;
+    drt3d_status s = make_plan(0, N, mask, o, P);
+    if (s != DRT3D_OK) return s;
+    if (P.small) return DRT3D_ERR_UNSUPPORTED;
+    s = check_ptrs(cube, r, workspace, workspace_bytes, P, o, 0);
+    if (s != DRT3D_OK) return s;
+    return run_drt(cube, mask, r, o, P, workspace, reinterpret_cast<cudaStream_t>(stream), true);
+}
+}  // namespace d3

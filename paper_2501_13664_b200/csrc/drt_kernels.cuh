@@ -58,6 +58,8 @@ struct DrtPass {
     int next_k;                     // non-final passes: radix bits of the pass that reads this output
     int inst_total;                 // instances (cubes x dodecants) of the whole call
     int tma_store;                  // final pass: emit the output tile with one TMA tensor store
+    int reduce_sub;                 // final fp32 pass: out <- out - A f (TMA reduce-add of -acc; the
+                                    // inverse's residual update, invert.cu), zero tiles add nothing
     uint32_t one;                   // = 1; a runtime multiplier so some adds issue as IMAD (FMA pipe)
     // zero tiles of the final output written by the first pass (DESIGN.md §5 item 6): the first
     // pass (zf_T > 0) writes the final pass's tiles of width zf_T that lie wholly below the support
@@ -302,6 +304,7 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
         const int s1max = (sg1 << K) + S - 1, s2max = (sg2 << K) + S - 1;
         if (Dabs + T <= 2 * N - s1max - s2max) {
             if (p.zeros_by_first) return;                // already written by the first pass
+            if (p.reduce_sub) return;                    // out - 0 = out
 #ifndef D3_ZERO_TMA
 #define D3_ZERO_TMA 1
 #endif
@@ -828,6 +831,14 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
 #ifndef D3_Y8_STORE_SWAP
 #define D3_Y8_STORE_SWAP 1
 #endif
+                if constexpr (std::is_same<Acc, float>::value) {
+                    if (p.reduce_sub) {                  // the tile is added to out: -acc
+#pragma unroll
+                        for (int r2 = 0; r2 < S; ++r2)
+#pragma unroll
+                            for (int j = 0; j < R; ++j) acc[r2][j] = -acc[r2][j];
+                    }
+                }
                 if constexpr ((Y8 || G::NRY == 8) && R == 8 && D3_Y8_STORE_SWAP) {
                     // runs 4.. write their two chunks in the opposite order: with runs 0..3 they
                     // then cover 8 distinct bank groups per store instruction of a quarter-warp
@@ -864,10 +875,16 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
                     "r"(d0), "r"(sg2 << K), "r"(sg1 << K), "r"(inst), "r"(src), "l"(pol)
                     : "memory");
 #else
-                asm volatile(
-                    "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(&omap),
-                    "r"(d0), "r"(sg2 << K), "r"(sg1 << K), "r"(inst), "r"(src)
-                    : "memory");
+                if (std::is_same<Acc, float>::value && p.reduce_sub)
+                    asm volatile(
+                        "cp.reduce.async.bulk.tensor.4d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(&omap),
+                        "r"(d0), "r"(sg2 << K), "r"(sg1 << K), "r"(inst), "r"(src)
+                        : "memory");
+                else
+                    asm volatile(
+                        "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(&omap),
+                        "r"(d0), "r"(sg2 << K), "r"(sg1 << K), "r"(inst), "r"(src)
+                        : "memory");
 #endif
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");

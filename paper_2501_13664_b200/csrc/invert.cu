@@ -23,6 +23,9 @@
 #include <cuda_runtime.h>
 
 namespace d3 {
+// api.cu: r <- r - A f (fp32, stacked) with the residual folded into the forward's final pass
+drt3d_status planes_residual(const void *cube, int N, uint32_t mask, float *r, const drt3d_opts *opts,
+                             void *workspace, size_t workspace_bytes, void *stream);
 namespace inv {
 
 constexpr int kRedBlocks = 1184;     // 8 x 148 SMs, fixed so the reduction order is fixed
@@ -345,11 +348,22 @@ drt3d_status mg_apply(Ctx &c, int l) {
         prolong_cube<<<(unsigned)(v.n * v.n), row_threads(v.n), 0, c.st>>>(c.f(u.e), c.f(v.e), v.n);        // e = P e_c
         int l1 = 0;
         c.o.launches = &l1;
-        s = drt3d_planes(c.f(v.e), v.n, c.mask, c.f(v.ae), &c.o, c.tws(), c.L->tws_bytes, c.stream);       // A e
-        if (s != DRT3D_OK) return s;
-        diff<<<nb, kRedThreads, 0, c.st>>>(c.f(v.r), c.f(v.ae), c.f(v.rp), v.ncoef);                        // r' = r - A e
-        c.nl += l1 + 2;
-        rem = c.f(v.rp);
+        // r' = r - A e, in place in r (r is not used again at this level): the forward's final pass
+        // adds -A e into r; small levels take A e and an elementwise difference
+        s = d3::planes_residual(c.f(v.e), v.n, c.mask, c.f(v.r), &c.o, c.tws(), c.L->tws_bytes, c.stream);
+        if (s == DRT3D_OK) {
+            c.nl += l1 + 1;
+            rem = c.f(v.r);
+        } else if (s == DRT3D_ERR_UNSUPPORTED) {
+            l1 = 0;
+            s = drt3d_planes(c.f(v.e), v.n, c.mask, c.f(v.ae), &c.o, c.tws(), c.L->tws_bytes, c.stream);   // A e
+            if (s != DRT3D_OK) return s;
+            diff<<<nb, kRedThreads, 0, c.st>>>(c.f(v.r), c.f(v.ae), c.f(v.rp), v.ncoef);                    // r' = r - A e
+            c.nl += l1 + 2;
+            rem = c.f(v.rp);
+        } else {
+            return s;
+        }
     } else {
         if (cudaMemsetAsync(c.f(v.e), 0, v.ncube * 4, c.st) != cudaSuccess) return DRT3D_ERR_CUDA;
     }

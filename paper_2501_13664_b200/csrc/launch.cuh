@@ -32,14 +32,15 @@ inline PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 }
 
 // 4D map of the stacked DRT output out[inst][s1][s2][3N] (32-bit), box {T, S, S1, 1}
-inline bool make_out_map(CUtensorMap *m, void *out, int N, int inst_total, int T, int S, int S1) {
+inline bool make_out_map(CUtensorMap *m, void *out, int N, int inst_total, int T, int S, int S1,
+                         CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_UINT32) {
     auto enc = tmap_encoder();
     if (!enc) return false;
     const cuuint64_t W = 3ull * N;
     cuuint64_t dims[4] = {W, (cuuint64_t)N, (cuuint64_t)N, (cuuint64_t)inst_total};
     cuuint64_t str[3] = {W * 4, W * 4 * N, W * 4 * N * N};
     cuuint32_t box[4] = {(cuuint32_t)T, (cuuint32_t)S, (cuuint32_t)S1, 1}, es[4] = {1, 1, 1, 1};
-    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, out, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+    return enc(m, dt, 4, out, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
            CUDA_SUCCESS;
 }
@@ -125,9 +126,16 @@ drt3d_status launch_drt_k(const DrtPass &prm_in, int ninst, cudaStream_t st) {
             make_out_map(&omap, prm.out, prm.N, prm.inst_total, T, S,
                          drt_warp_store<K, R, T, !FIRST && sizeof(In) == 2, FINAL>()    ? 4
                          : drt_hybrid_store<K, R, T, !FIRST && sizeof(In) == 2, FINAL>() ? S / 2
-                                                                                        : S))
+                                                                                        : S,
+                         std::is_same<Out, float>::value ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                                         : CU_TENSOR_MAP_DATA_TYPE_UINT32))
             prm.tma_store = 1;
     }
+    // the in-place residual (out <- out - A f) needs the fp32 CTA-wide TMA reduce path
+    if (prm.reduce_sub && !(FINAL && std::is_same<Out, float>::value && prm.tma_store &&
+                            !drt_warp_store<K, R, T, !FIRST && sizeof(In) == 2, FINAL>() &&
+                            !drt_hybrid_store<K, R, T, !FIRST && sizeof(In) == 2, FINAL>()))
+        return DRT3D_ERR_UNSUPPORTED;
     if constexpr (!FIRST && D3_PDL) {
         // programmatic dependent launch: scheduled while the previous kernel on the stream finishes
         cudaLaunchConfig_t cfg{};
