@@ -59,6 +59,21 @@ def test_multigrid_matches_oracle(N, mask, iters, n_min):
     assert np.allclose(rn, rn_ref, rtol=1e-4, atol=0)
 
 
+def test_multigrid_n64_residual_in_forward():
+    """N = 64 (top level above the on-chip sizes): the residual update r <- r - A e runs inside the
+    forward's final pass (TMA reduce-add, invert.cu / api.cu planes_residual); against the fp64
+    oracle iteration within T3."""
+    N = 64
+    f = _phantom(N)
+    b = oracle.drt_planes(f, 0xFFF)
+    x_ref, rn_ref = inv.press_multigrid(b, 2, 0xFFF, n_min=16)
+    x, rn = d3.planes_invert(torch.from_numpy(b.astype(np.float32)).cuda(), 2, 0xFFF, n_min=16)
+    torch.cuda.synchronize()
+    x, rn = x.cpu().numpy().astype(np.float64), rn.cpu().numpy()
+    assert np.max(np.abs(x - x_ref)) <= 1e-4 * np.max(np.abs(x_ref))
+    assert np.allclose(rn, rn_ref, rtol=1e-4, atol=0)
+
+
 def test_invert_random_cube():
     N = 8
     f = synth.normal_cube(N, 77).astype(np.float64)
