@@ -296,6 +296,40 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
         outp[(long long)b * 16 * N * N * (3 * N - 2) + rr * (3 * N - 2) + D - 2] = to_out<Out, Acc>(v);
     };
     const bool mosaic = FINAL && p.layout == 1;
+    // mosaic row of slopes (r1, r2) of this group: [b][4N][4N][3N - 2], element d = D - 2 (8-byte
+    // aligned: the row pitch 3N - 2 and the run starts D0 - 2 are even)
+    auto mosaic_row = [&](int r1, int r2) -> Out * {
+        const int b = inst / p.ndod, j = inst - b * p.ndod;
+        const int s[2] = {(sg1 << K) + r1, (sg2 << K) + r2};
+        const int o0 = p.out_order[j][0], o1 = p.out_order[j][1];
+        int w0 = s[(o0 < 0 ? -o0 : o0) - 1], w1 = s[(o1 < 0 ? -o1 : o1) - 1];
+        if (o0 < 0) w0 = N - 1 - w0;
+        if (o1 < 0) w1 = N - 1 - w1;
+        const long long rr = (long long)(p.coords[j][0] * N + w0) * (4 * N) + (p.coords[j][1] * N + w1);
+        return outp + (long long)b * 16 * N * N * (3 * N - 2) + rr * (3 * N - 2);
+    };
+    // elements [D0, D0 + n) of a mosaic row from registers v[0..n) (n even, D0 even): pairs as 8-byte
+    // stores, D < 2 and D >= 3N dropped
+    auto mosaic_run = [&](Out *row, int D0, const uint32_t *v, int n) {
+        if (n == 8 && D0 >= 2 && D0 + 8 <= p.out_width) {
+            // interior run of 8: 16-byte stores where the address allows (it is 8-byte aligned)
+            unsigned char *dst = reinterpret_cast<unsigned char *>(row + D0 - 2);
+            if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+                *reinterpret_cast<uint4 *>(dst) = make_uint4(v[0], v[1], v[2], v[3]);
+                *reinterpret_cast<uint4 *>(dst + 16) = make_uint4(v[4], v[5], v[6], v[7]);
+            } else {
+                *reinterpret_cast<uint2 *>(dst) = make_uint2(v[0], v[1]);
+                *reinterpret_cast<uint4 *>(dst + 8) = make_uint4(v[2], v[3], v[4], v[5]);
+                *reinterpret_cast<uint2 *>(dst + 24) = make_uint2(v[6], v[7]);
+            }
+            return;
+        }
+        for (int q = 0; q < n; q += 2) {
+            const int D = D0 + q;
+            if (D >= 2 && D + 2 <= p.out_width)
+                *reinterpret_cast<uint2 *>(row + D - 2) = make_uint2(v[q], v[q + 1]);
+        }
+    };
 
     // ---- final tiles entirely outside the support of all 4^K output rows: zeros
     // (support D >= 2N - s1 - s2).  Intermediate tiles are always computed so
@@ -342,6 +376,17 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
                     else *reinterpret_cast<uint4 *>(dst) = make_uint4(0u, 0u, 0u, 0u);
                 }
             } else {
+                if (mosaic && (T % 2) == 0 && (d0 % 2) == 0) {
+                    // zero runs of 8 (or the tile's tail) per mosaic row, 8-byte stores
+                    constexpr int RUN = 8;
+                    const uint32_t z[RUN] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+                    for (int i = tid; i < S * S * ((T + RUN - 1) / RUN); i += blockDim.x) {
+                        const int rr = i / ((T + RUN - 1) / RUN), q = i - rr * ((T + RUN - 1) / RUN);
+                        const int n = T - RUN * q < RUN ? T - RUN * q : RUN;
+                        mosaic_run(mosaic_row(rr / S, rr % S), d0 + RUN * q, z, n);
+                    }
+                    return;
+                }
                 for (int i = tid; i < S * S * T; i += blockDim.x) {
                     const int rr = i / T, e = i - rr * T;
                     if (mosaic) store_mosaic(rr / S, rr % S, e, Acc(0));
@@ -911,9 +956,19 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
         const int r1 = yb, e0 = yr * R;
         if (mosaic) {
 #pragma unroll
-            for (int r2 = 0; r2 < S; ++r2)
+            for (int r2 = 0; r2 < S; ++r2) {
+                if constexpr (R % 2 == 0) {
+                    if ((d0 % 2) == 0) {
+                        uint32_t v[R];
+#pragma unroll
+                        for (int j = 0; j < R; ++j) v[j] = Lane<Acc>::bits(acc[r2][j]);
+                        mosaic_run(mosaic_row(r1, r2), d0 + e0, v, R);
+                        continue;
+                    }
+                }
 #pragma unroll
                 for (int j = 0; j < R; ++j) store_mosaic(r1, r2, e0 + j, acc[r2][j]);
+            }
             return;
         }
         const bool vec_ok = (d0 + e0 + R <= p.out_width) && ((p.out_pitch * (int)sizeof(Out)) % 16 == 0) &&
