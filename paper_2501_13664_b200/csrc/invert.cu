@@ -203,13 +203,13 @@ inline size_t align256(size_t b) { return (b + 255) / 256 * 256; }
 
 constexpr int kMaxLevels = 11;
 
-// Per grid level (0 = the caller's size N, level l has size N >> l): residual r, its remainder
-// rp = r - A e, and A e / A p sharing one buffer (coefficient-sized); e, A^T rp, p (cube-sized).
-// Level 0's r is the outer residual.
+// Per grid level (0 = the caller's size N, level l has size N >> l): residual r (its remainder
+// r - A e replaces it in place), and A e / A p sharing one buffer (coefficient-sized); e, A^T r, p
+// (cube-sized).  Level 0's r is the outer residual.
 struct Level {
     int n;
     size_t ncoef, ncube;
-    size_t r, rp, ae, q, e, g, p;
+    size_t r, ae, q, e, g, p;
 };
 
 struct Layout {
@@ -245,7 +245,6 @@ inline drt3d_status layout(int N, int n_min, uint32_t mask, int table, Layout &L
         v.ncoef = (size_t)K * n * n * 3 * n;
         v.ncube = (size_t)n * n * n;
         v.r = off; off += align256(v.ncoef * 4);
-        v.rp = off; off += align256(v.ncoef * 4);
         v.q = off; off += align256(v.ncoef * 4);
         v.ae = v.q;                                     // A e is dead once r' = r - A e is formed
         v.e = off; off += align256(v.ncube * 4);
@@ -358,9 +357,9 @@ drt3d_status mg_apply(Ctx &c, int l) {
             l1 = 0;
             s = drt3d_planes(c.f(v.e), v.n, c.mask, c.f(v.ae), &c.o, c.tws(), c.L->tws_bytes, c.stream);   // A e
             if (s != DRT3D_OK) return s;
-            diff<<<nb, kRedThreads, 0, c.st>>>(c.f(v.r), c.f(v.ae), c.f(v.rp), v.ncoef);                    // r' = r - A e
+            diff<<<nb, kRedThreads, 0, c.st>>>(c.f(v.r), c.f(v.ae), c.f(v.r), v.ncoef);                     // r' = r - A e
             c.nl += l1 + 2;
-            rem = c.f(v.rp);
+            rem = c.f(v.r);
         } else {
             return s;
         }
