@@ -466,8 +466,8 @@ struct JoinGuard {
 // Each instance has its own stage buffer slice inside the chunk, so groups never wait on each
 // other's buffers; consecutive chunks of large batches alternate between two buffer sets.
 drt3d_status run_drt(const void *cube, uint32_t mask, void *out, const drt3d_opts &o, const Plan &P, void *ws,
-                     cudaStream_t st, bool reduce_sub = false) {
-    if (reduce_sub && (P.small || o.layout != DRT3D_LAYOUT_STACKED || o.out_dtype != DRT3D_F32))
+                     cudaStream_t st, bool reduce_sub = false, double *sq_part = nullptr, int *sq_count = nullptr) {
+    if ((reduce_sub || sq_part) && (P.small || o.layout != DRT3D_LAYOUT_STACKED || o.out_dtype != DRT3D_F32))
         return DRT3D_ERR_UNSUPPORTED;
     const int8_t(*rows)[3] = table_rows(o.table, 0);
     DrtPass base{};
@@ -556,6 +556,8 @@ drt3d_status run_drt(const void *cube, uint32_t mask, void *out, const drt3d_opt
                 }
                 if (zfirst && fin) prm.zeros_by_first = 1;
                 prm.reduce_sub = (reduce_sub && fin) ? 1 : 0;
+                prm.sq_part = fin ? sq_part : nullptr;
+                prm.sq_count = fin ? sq_count : nullptr;
                 drt3d_status s = DRT3D_OK;
                 drt3d_status ls = L.run_on(ps, first ? 0 : (fin ? 2 : 1), [&] {
                     s = dispatch_drt(o.in_dtype, P.ks[p], P.stor[p], P.stor[p + 1], first, fin, prm, gn, ps);
@@ -867,5 +869,29 @@ drt3d_status planes_residual(const void *cube, int N, uint32_t mask, float *r, c
     s = check_ptrs(cube, r, workspace, workspace_bytes, P, o, 0);
     if (s != DRT3D_OK) return s;
     return run_drt(cube, mask, r, o, P, workspace, reinterpret_cast<cudaStream_t>(stream), true);
+}
+
+// Internal entry: out = A f (fp32, stacked) and, fused into the final pass, per-CTA sums of out^2 in
+// fp64 at sq_part[0 .. *sq_count) (the count is written by the kernel; at most
+// planes_sumsq_parts(N, batch x dodecants) entries).  DRT3D_ERR_UNSUPPORTED, nothing enqueued, as for
+// planes_residual.
+size_t planes_sumsq_parts(int N, int instances) {
+    // final passes with K >= 2: groups x tiles <= N^2 / 16 x 3N / 96 (the smallest group and tile)
+    return (size_t)instances * N * N / 16 * ((3 * (size_t)N + 95) / 96) + 1;
+}
+drt3d_status planes_sumsq(const void *cube, int N, uint32_t mask, float *out, const drt3d_opts *opts,
+                          void *workspace, size_t workspace_bytes, void *stream, double *sq_part, int *sq_count) {
+    drt3d_opts tmp;
+    const drt3d_opts &o = opts_or_default(opts, tmp);
+    if (o.in_dtype != DRT3D_F32 || o.out_dtype != DRT3D_F32 || o.layout != DRT3D_LAYOUT_STACKED || N < 64 || !sq_part ||
+        !sq_count)
+        return DRT3D_ERR_UNSUPPORTED;
+    Plan P;
+    drt3d_status s = make_plan(0, N, mask, o, P);
+    if (s != DRT3D_OK) return s;
+    if (P.small) return DRT3D_ERR_UNSUPPORTED;
+    s = check_ptrs(cube, out, workspace, workspace_bytes, P, o, 0);
+    if (s != DRT3D_OK) return s;
+    return run_drt(cube, mask, out, o, P, workspace, reinterpret_cast<cudaStream_t>(stream), false, sq_part, sq_count);
 }
 }  // namespace d3

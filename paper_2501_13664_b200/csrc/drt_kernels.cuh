@@ -60,6 +60,9 @@ struct DrtPass {
     int tma_store;                  // final pass: emit the output tile with one TMA tensor store
     int reduce_sub;                 // final fp32 pass: out <- out - A f (TMA reduce-add of -acc; the
                                     // inverse's residual update, invert.cu), zero tiles add nothing
+    double *sq_part;                // final fp32 pass: per-CTA sum of out^2 (fp64) at
+                                    // sq_part[(inst * gridDim.y + y) * gridDim.x + x], count in sq_count
+    int *sq_count;
     uint32_t one;                   // = 1; a runtime multiplier so some adds issue as IMAD (FMA pipe)
     // zero tiles of the final output written by the first pass (DESIGN.md §5 item 6): the first
     // pass (zf_T > 0) writes the final pass's tiles of width zf_T that lie wholly below the support
@@ -337,6 +340,10 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
     if constexpr (FINAL) {
         const int s1max = (sg1 << K) + S - 1, s2max = (sg2 << K) + S - 1;
         if (Dabs + T <= 2 * N - s1max - s2max) {
+            if (p.sq_part && tid == 0) {
+                p.sq_part[((long long)inst * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = 0.0;
+                if (blockIdx.x == 0 && blockIdx.y == 0 && li == 0) *p.sq_count = p.inst_total * (int)(gridDim.x * gridDim.y);
+            }
             if (p.zeros_by_first) return;                // already written by the first pass
             if (p.reduce_sub) return;                    // out - 0 = out
 #ifndef D3_ZERO_TMA
@@ -870,6 +877,8 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
         }
     } else if constexpr (FINAL && sizeof(Out) == 4) {
         if (p.tma_store) {
+            __shared__ double sq_warp[32];
+            double sq_thread = 0.0;
             __syncthreads();                                 // every y-step read of X is done
             if (yact) {
                 unsigned char *row = sm + ((yb * S) * T + yr * R) * 4;
@@ -877,6 +886,14 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
 #define D3_Y8_STORE_SWAP 1
 #endif
                 if constexpr (std::is_same<Acc, float>::value) {
+                    if (p.sq_part) {                     // this thread's share of sum out^2 (fp64, fixed order)
+                        double ss = 0.0;
+#pragma unroll
+                        for (int r2 = 0; r2 < S; ++r2)
+#pragma unroll
+                            for (int j = 0; j < R; ++j) ss += (double)acc[r2][j] * (double)acc[r2][j];
+                        sq_thread = ss;
+                    }
                     if (p.reduce_sub) {                  // the tile is added to out: -acc
 #pragma unroll
                         for (int r2 = 0; r2 < S; ++r2)
@@ -908,8 +925,19 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
                                            Lane<Acc>::bits(acc[r2][4 * q + 2]), Lane<Acc>::bits(acc[r2][4 * q + 3]));
                 }
             }
+            if (std::is_same<Acc, float>::value && p.sq_part) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) sq_thread += __shfl_xor_sync(0xffffffffu, sq_thread, o);
+                if ((tid & 31) == 0) sq_warp[tid >> 5] = sq_thread;
+            }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncthreads();
+            if (std::is_same<Acc, float>::value && p.sq_part && tid == 0) {
+                double t = 0.0;
+                for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sq_warp[w];
+                p.sq_part[((long long)inst * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
+                if (blockIdx.x == 0 && blockIdx.y == 0 && li == 0) *p.sq_count = p.inst_total * (int)(gridDim.x * gridDim.y);
+            }
             if (tid == 0) {
                 const uint32_t src = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
 #ifdef D3_TMA_EVICT_FIRST

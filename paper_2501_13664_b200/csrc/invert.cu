@@ -26,6 +26,10 @@ namespace d3 {
 // api.cu: r <- r - A f (fp32, stacked) with the residual folded into the forward's final pass
 drt3d_status planes_residual(const void *cube, int N, uint32_t mask, float *r, const drt3d_opts *opts,
                              void *workspace, size_t workspace_bytes, void *stream);
+// api.cu: out = A f (fp32, stacked) with per-CTA sums of out^2 fused into the final pass
+size_t planes_sumsq_parts(int N, int instances);
+drt3d_status planes_sumsq(const void *cube, int N, uint32_t mask, float *out, const drt3d_opts *opts,
+                          void *workspace, size_t workspace_bytes, void *stream, double *sq_part, int *sq_count);
 namespace inv {
 
 constexpr int kRedBlocks = 1184;     // 8 x 148 SMs, fixed so the reduction order is fixed
@@ -76,6 +80,20 @@ __global__ void finalize_alpha(const double *__restrict__ part, int nb, double *
     }
     const double s0 = block_sum(rq, sh[0]);
     const double s1 = block_sum(qq, sh[1]);
+    if (threadIdx.x == 0) *alpha = s1 > 0.0 ? s0 / s1 : 0.0;
+}
+
+// alpha = <g, p> / <q, q>: <g, p> = sum part[2i] (dot_rq_qq(g, p) partials; <r, A p> = <A^T r, p>
+// with g = A^T r), <q, q> = sum qq[0 .. *count) (the forward's per-CTA sums), both in a fixed order
+__global__ void finalize_alpha_gp(const double *__restrict__ part, int nb, const double *__restrict__ qq,
+                                  const int *__restrict__ count, double *__restrict__ alpha) {
+    __shared__ double sh[2][kRedThreads / 32];
+    double gp = 0.0, q2 = 0.0;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) gp += part[2 * i];
+    const int n = *count;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) q2 += qq[i];
+    const double s0 = block_sum(gp, sh[0]);
+    const double s1 = block_sum(q2, sh[1]);
     if (threadIdx.x == 0) *alpha = s1 > 0.0 ? s0 / s1 : 0.0;
 }
 
@@ -215,7 +233,7 @@ struct Level {
 struct Layout {
     int nlev;
     Level lv[kMaxLevels];
-    size_t part, scal, tws, total, tws_bytes;
+    size_t part, scal, tws, total, tws_bytes, qq, qq_cap;
 };
 
 inline drt3d_opts f32_opts(int table) {
@@ -252,6 +270,8 @@ inline drt3d_status layout(int N, int n_min, uint32_t mask, int table, Layout &L
         v.p = off; off += align256(v.ncube * 4);
     }
     L.part = off; off += align256(2 * kRedBlocks * sizeof(double));
+    L.qq_cap = planes_sumsq_parts(N, K);                // per-CTA sums of (A p)^2 of the largest level
+    L.qq = off; off += align256(L.qq_cap * sizeof(double) + 256);
     L.scal = off; off += 256;                           // [0] = 1.0, [1 + l] = alpha of level l, int at +128
     static_assert(8 * (1 + kMaxLevels) <= 128, "scalar slots");
     L.tws = off; off += L.tws_bytes;
@@ -303,6 +323,8 @@ struct Ctx {
     double *rnorm;
     float *f(size_t off) const { return reinterpret_cast<float *>(w + off); }
     double *part() const { return reinterpret_cast<double *>(w + L->part); }
+    double *qq() const { return reinterpret_cast<double *>(w + L->qq); }
+    int *qq_count() const { return reinterpret_cast<int *>(w + L->qq + L->qq_cap * sizeof(double)); }
     double *one() const { return reinterpret_cast<double *>(w + L->scal); }
     double *alpha(int l) const { return reinterpret_cast<double *>(w + L->scal) + 1 + l; }
     int *ctr() const { return reinterpret_cast<int *>(w + L->scal + 128); }
@@ -320,6 +342,17 @@ drt3d_status step(Ctx &c, int l, const float *res) {
     if (s != DRT3D_OK) return s;
     highpass<<<(unsigned)(v.n * v.n), row_threads(v.n), 0, c.st>>>(c.f(v.g), c.f(v.p), v.n);
     c.o.launches = &l2;
+    // q = A p with <q, q> summed in the forward's final pass, <res, q> = <A^T res, p> = <g, p> over the
+    // cube: no pass over the coefficients (N >= 64); smaller levels take the coefficient-sized dot
+    s = d3::planes_sumsq(c.f(v.p), v.n, c.mask, c.f(v.q), &c.o, c.tws(), c.L->tws_bytes, c.stream, c.qq(), c.qq_count());
+    if (s == DRT3D_OK) {
+        dot_rq_qq<<<kRedBlocks, kRedThreads, 0, c.st>>>(c.f(v.g), c.f(v.p), v.ncube, c.part());
+        finalize_alpha_gp<<<1, kRedThreads, 0, c.st>>>(c.part(), kRedBlocks, c.qq(), c.qq_count(), c.alpha(l));
+        c.nl += l1 + l2 + 3;
+        return DRT3D_OK;
+    }
+    if (s != DRT3D_ERR_UNSUPPORTED) return s;
+    l2 = 0;
     s = drt3d_planes(c.f(v.p), v.n, c.mask, c.f(v.q), &c.o, c.tws(), c.L->tws_bytes, c.stream);
     if (s != DRT3D_OK) return s;
     dot_rq_qq<<<kRedBlocks, kRedThreads, 0, c.st>>>(res, c.f(v.q), v.ncoef, c.part());

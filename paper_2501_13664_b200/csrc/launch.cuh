@@ -132,7 +132,7 @@ drt3d_status launch_drt_k(const DrtPass &prm_in, int ninst, cudaStream_t st) {
             prm.tma_store = 1;
     }
     // the in-place residual (out <- out - A f) needs the fp32 CTA-wide TMA reduce path
-    if (prm.reduce_sub && !(FINAL && std::is_same<Out, float>::value && prm.tma_store &&
+    if ((prm.reduce_sub || prm.sq_part) && !(FINAL && std::is_same<Out, float>::value && prm.tma_store &&
                             !drt_warp_store<K, R, T, !FIRST && sizeof(In) == 2, FINAL>() &&
                             !drt_hybrid_store<K, R, T, !FIRST && sizeof(In) == 2, FINAL>()))
         return DRT3D_ERR_UNSUPPORTED;
