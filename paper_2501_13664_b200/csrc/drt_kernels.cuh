@@ -497,39 +497,67 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
             // and transposed in registers (reversed axes: the 4 values in reverse order).
             constexpr int NQ4 = BW / 4;
             if (o.fast == 2) {
-                for (int it = tid; it < S * S * NQ4; it += blockDim.x) {
-                    const int slot = it / NQ4, q = it - slot * NQ4;
-                    const int w1 = slot / S, w2 = slot - w1 * S, z = z0 + 4 * q;
-                    uint4 v = make_uint4(0u, 0u, 0u, 0u);
-                    if ((unsigned)z < (unsigned)N)
-                        v = __ldg(reinterpret_cast<const uint4 *>(cube + o.off0 + (long long)(xb + w1) * o.sx +
-                                                                  (long long)(yb + w2) * o.sy + z));
-                    put4(slot, q, v);
+                // ITEMS independent loads in flight per thread before any is stored (one load per
+                // iteration left each thread waiting a full L2 round trip per chunk)
+                constexpr int ITEMS = 8;
+                for (int base = tid; base < S * S * NQ4; base += blockDim.x * ITEMS) {
+                    uint4 v[ITEMS];
+#pragma unroll
+                    for (int u = 0; u < ITEMS; ++u) {
+                        const int it = base + u * blockDim.x;
+                        const int slot = it / NQ4, q = it - slot * NQ4;
+                        const int w1 = slot / S, w2 = slot - w1 * S, z = z0 + 4 * q;
+                        v[u] = make_uint4(0u, 0u, 0u, 0u);
+                        if (it < S * S * NQ4 && (unsigned)z < (unsigned)N)
+                            v[u] = __ldg(reinterpret_cast<const uint4 *>(cube + o.off0 + (long long)(xb + w1) * o.sx +
+                                                                         (long long)(yb + w2) * o.sy + z));
+                    }
+#pragma unroll
+                    for (int u = 0; u < ITEMS; ++u) {
+                        const int it = base + u * blockDim.x;
+                        if (it < S * S * NQ4) put4(it / NQ4, it - (it / NQ4) * NQ4, v[u]);
+                    }
                 }
             } else {
                 const bool fy = o.fast == 1;
                 const long long sf = fy ? o.sy : o.sx, so = fy ? o.sx : o.sy;
                 const int fb = fy ? yb : xb, ob = fy ? xb : yb;
-                for (int it = tid; it < S * (S / 4) * NQ4; it += blockDim.x) {
-                    const int q = it % NQ4, rest = it / NQ4, g4 = rest % (S / 4), other = rest / (S / 4);
-                    uint32_t v[4][4];
+                // two items (8 loads) in flight per thread before any is stored
+                constexpr int ITEMS = 2;
+                for (int base = tid; base < S * (S / 4) * NQ4; base += blockDim.x * ITEMS) {
+                    uint4 a[ITEMS][4];
 #pragma unroll
-                    for (int t = 0; t < 4; ++t) {
-                        const int z = z0 + 4 * q + t;
-                        uint4 a = make_uint4(0u, 0u, 0u, 0u);
-                        if ((unsigned)z < (unsigned)N) {
-                            const long long b = o.off0 + (long long)(ob + other) * so + (long long)z * o.sz +
-                                                (sf > 0 ? (long long)(fb + 4 * g4) : -(long long)(fb + 4 * g4 + 3));
-                            a = __ldg(reinterpret_cast<const uint4 *>(cube + b));
+                    for (int u = 0; u < ITEMS; ++u) {
+                        const int it = base + u * blockDim.x;
+                        const int q = it % NQ4, rest = it / NQ4, g4 = rest % (S / 4), other = rest / (S / 4);
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) {
+                            const int z = z0 + 4 * q + t;
+                            a[u][t] = make_uint4(0u, 0u, 0u, 0u);
+                            if (it < S * (S / 4) * NQ4 && (unsigned)z < (unsigned)N) {
+                                const long long b = o.off0 + (long long)(ob + other) * so + (long long)z * o.sz +
+                                                    (sf > 0 ? (long long)(fb + 4 * g4) : -(long long)(fb + 4 * g4 + 3));
+                                a[u][t] = __ldg(reinterpret_cast<const uint4 *>(cube + b));
+                            }
                         }
-                        const uint32_t av[4] = {a.x, a.y, a.z, a.w};
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) v[t][j] = av[sf > 0 ? j : 3 - j];
                     }
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const int f = 4 * g4 + j;
-                        put4(fy ? other * S + f : f * S + other, q, make_uint4(v[0][j], v[1][j], v[2][j], v[3][j]));
+                    for (int u = 0; u < ITEMS; ++u) {
+                        const int it = base + u * blockDim.x;
+                        if (it >= S * (S / 4) * NQ4) break;
+                        const int q = it % NQ4, rest = it / NQ4, g4 = rest % (S / 4), other = rest / (S / 4);
+                        uint32_t v[4][4];
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) {
+                            const uint32_t av[4] = {a[u][t].x, a[u][t].y, a[u][t].z, a[u][t].w};
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) v[t][j] = av[sf > 0 ? j : 3 - j];
+                        }
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const int f = 4 * g4 + j;
+                            put4(fy ? other * S + f : f * S + other, q, make_uint4(v[0][j], v[1][j], v[2][j], v[3][j]));
+                        }
                     }
                 }
             }
