@@ -63,8 +63,16 @@ struct DjtGeom {
 #define D3_DJT_OUT_TMA 0                  // measured: cfg4 0.0891 vs 0.0860 ms with the direct 16-byte stores
 #endif
     static constexpr bool OUT_TMA = D3_DJT_OUT_TMA && T1 * NR == 32 && THREADS % 32 == 0 && R == 8;
+    // final passes (D3_DJT_OUT_SMEM): a warp's tasks (one r1, T1 = 8 rows x T2 = 32 columns, S planes)
+    // go through a per-warp XOR-swizzled shared-memory image, so that every 16-byte store instruction
+    // writes 4 whole 128-byte row segments (direct stores from the task registers put 16 bytes in
+    // each of 32 sectors of 8 lines per instruction: the L1 data pipe was at 81% on cfg4)
+#ifndef D3_DJT_OUT_SMEM
+#define D3_DJT_OUT_SMEM 1
+#endif
+    static constexpr bool OUT_SMEM = D3_DJT_OUT_SMEM && !OUT_TMA && T1 == 8 && T2 == 32 && R == 8 && THREADS % 32 == 0;
     static constexpr int IMG = S * T1 * T2 * 4;
-    static constexpr int SMEM = SMEM_STAGE + (OUT_TMA ? (THREADS / 32) * IMG : 0);
+    static constexpr int SMEM = SMEM_STAGE + ((OUT_TMA || OUT_SMEM) ? (THREADS / 32) * IMG : 0);
     static_assert(T2 % R == 0 && R % 4 == 0, "tile shape");
 };
 
@@ -283,6 +291,34 @@ djt_pass_kernel(const DjtPass p, const __grid_constant__ CUtensorMap zmap) {
                     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                 }
                 __syncwarp();
+                continue;
+            }
+        }
+        if constexpr (FINAL && sizeof(Out) == 4 && G::OUT_SMEM) {
+            if (d10 + T1 <= p.out_width && d20 + T2 <= p.out_width && (p.out_pitch % 4) == 0 && (d20 % 4) == 0 &&
+                (p.out_plane % 4) == 0) {
+                // image rows (r2, d1) of 8 chunks; piece k = 2 rr + q of row d1 at chunk k ^ d1 (the 8
+                // lanes of a quarter-warp -- 8 rows d1 of one piece, or 8 pieces of one row -- touch 8
+                // distinct 16-byte bank groups both ways)
+                uint4 *img = reinterpret_cast<uint4 *>(reinterpret_cast<unsigned char *>(smem_u4) + G::SMEM_STAGE +
+                                                       (tid >> 5) * G::IMG);
+                __syncwarp();                               // the previous iteration's reads are done
+#pragma unroll
+                for (int r2 = 0; r2 < S; ++r2)
+#pragma unroll
+                    for (int q = 0; q < 2; ++q)
+                        img[(r2 * T1 + d1) * 8 + ((2 * rr + q) ^ d1)] =
+                            make_uint4(Lane<Acc>::bits(acc[r2][4 * q]), Lane<Acc>::bits(acc[r2][4 * q + 1]),
+                                       Lane<Acc>::bits(acc[r2][4 * q + 2]), Lane<Acc>::bits(acc[r2][4 * q + 3]));
+                __syncwarp();
+                const int lane = tid & 31, k = lane & 7;
+#pragma unroll
+                for (int it = 0; it < S * T1 / 4; ++it) {
+                    const int row = 4 * it + (lane >> 3), r2 = row / T1, e = row - r2 * T1;
+                    const uint4 v = img[row * 8 + (k ^ e)];
+                    Out *dst = out_plane_ptr(r1, r2) + (long long)(d10 + e) * p.out_pitch + d20 + 4 * k;
+                    st_cs_v4(dst, v.x, v.y, v.z, v.w);
+                }
                 continue;
             }
         }
