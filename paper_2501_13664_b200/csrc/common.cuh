@@ -220,6 +220,20 @@ __device__ __forceinline__ void st_cs_v4(void *p, uint32_t a, uint32_t b, uint32
     asm volatile("st.global.cs.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 
+// 32-byte global stores (STG.256, sm_100): a lane fills one whole 32-byte sector, so a warp's
+// scattered row stores need half the instructions (and L1 data-pipe wavefronts) of 16-byte ones.
+// p must be 32-byte aligned.
+__device__ __forceinline__ void st_cs_v8(void *p, const uint32_t (&v)[8]) {
+    asm volatile("st.global.cs.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+                 "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+__device__ __forceinline__ void st_v8(void *p, const uint32_t (&v)[8]) {
+    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+                 "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // Staging of row segments into shared memory with batched 16-byte loads.
 // Row r supplies elements j = st + dir*e, e in [0, W), of a contiguous source

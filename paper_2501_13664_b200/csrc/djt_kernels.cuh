@@ -70,7 +70,14 @@ struct DjtGeom {
 #ifndef D3_DJT_OUT_SMEM
 #define D3_DJT_OUT_SMEM 1
 #endif
-    static constexpr bool OUT_SMEM = D3_DJT_OUT_SMEM && !OUT_TMA && T1 == 8 && T2 == 32 && R == 8 && THREADS % 32 == 0;
+    // D3_DJT_ST256: final 32-bit outputs leave the task registers as 32-byte stores (STG.256): a
+    // lane's 8 columns fill one whole sector, 4 lanes one 128-byte line, so each instruction writes
+    // 8 whole lines with no shared-memory image
+#ifndef D3_DJT_ST256
+#define D3_DJT_ST256 0
+#endif
+    static constexpr bool OUT_SMEM =
+        D3_DJT_OUT_SMEM && !D3_DJT_ST256 && !OUT_TMA && T1 == 8 && T2 == 32 && R == 8 && THREADS % 32 == 0;
     static constexpr int IMG = S * T1 * T2 * 4;
     static constexpr int SMEM = SMEM_STAGE + ((OUT_TMA || OUT_SMEM) ? (THREADS / 32) * IMG : 0);
     static_assert(T2 % R == 0 && R % 4 == 0, "tile shape");
@@ -312,6 +319,23 @@ djt_pass_kernel(const DjtPass p, const __grid_constant__ CUtensorMap zmap) {
                                        Lane<Acc>::bits(acc[r2][4 * q + 2]), Lane<Acc>::bits(acc[r2][4 * q + 3]));
                 __syncwarp();
                 const int lane = tid & 31, k = lane & 7;
+#ifndef D3_DJT_IMG256
+#define D3_DJT_IMG256 0
+#endif
+                if (D3_DJT_IMG256 && (p.out_pitch % 8) == 0 && (p.out_plane % 8) == 0 && (p.out_inst_stride % 8) == 0 &&
+                    (reinterpret_cast<unsigned long long>(outp) & 31ull) == 0) {
+                    // 32-byte stores: 4 lanes per 128-byte row segment, 8 whole lines per instruction
+                    const int k2 = lane & 3;
+#pragma unroll
+                    for (int it = 0; it < S * T1 / 8; ++it) {
+                        const int row = 8 * it + (lane >> 2), r2 = row / T1, e = row - r2 * T1;
+                        const uint4 a = img[row * 8 + ((2 * k2) ^ e)], b = img[row * 8 + ((2 * k2 + 1) ^ e)];
+                        Out *dst = out_plane_ptr(r1, r2) + (long long)(d10 + e) * p.out_pitch + d20 + 8 * k2;
+                        const uint32_t v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+                        st_cs_v8(dst, v);
+                    }
+                    continue;
+                }
 #pragma unroll
                 for (int it = 0; it < S * T1 / 4; ++it) {
                     const int row = 4 * it + (lane >> 3), r2 = row / T1, e = row - r2 * T1;
@@ -327,6 +351,10 @@ djt_pass_kernel(const DjtPass p, const __grid_constant__ CUtensorMap zmap) {
         if (e1 < p.out_width) {
             const bool vec_ok = (e2 + R <= p.out_width) && ((p.out_pitch * (int)sizeof(Out)) % 16 == 0) &&
                                 ((e2 * (int)sizeof(Out)) % 16 == 0) && ((p.out_plane * (long long)sizeof(Out)) % 16 == 0);
+            [[maybe_unused]] const bool vec32_ok =
+                vec_ok && ((p.out_pitch * (int)sizeof(Out)) % 32 == 0) && ((e2 * (int)sizeof(Out)) % 32 == 0) &&
+                ((p.out_plane * (long long)sizeof(Out)) % 32 == 0) && ((p.out_inst_stride * (long long)sizeof(Out)) % 32 == 0) &&
+                ((reinterpret_cast<unsigned long long>(outp) & 31ull) == 0);
 #pragma unroll
             for (int r2 = 0; r2 < S; ++r2) {
                 Out *dst = out_plane_ptr(r1, r2) + (long long)e1 * p.out_pitch + e2;
@@ -342,6 +370,15 @@ djt_pass_kernel(const DjtPass p, const __grid_constant__ CUtensorMap zmap) {
                             *reinterpret_cast<uint4 *>(dst + 8 * q) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
                         }
                     } else {
+                        if constexpr (FINAL && R == 8 && D3_DJT_ST256) {
+                            if (vec32_ok) {
+                                uint32_t v[8];
+#pragma unroll
+                                for (int j = 0; j < 8; ++j) v[j] = Lane<Acc>::bits(acc[r2][j]);
+                                st_cs_v8(dst, v);
+                                continue;
+                            }
+                        }
 #pragma unroll
                         for (int q = 0; q < R / 4; ++q) {
                             const uint32_t a0 = Lane<Acc>::bits(acc[r2][4 * q + 0]), a1 = Lane<Acc>::bits(acc[r2][4 * q + 1]);

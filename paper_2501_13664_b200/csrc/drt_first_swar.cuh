@@ -475,11 +475,10 @@ drt_first_swar_kernel(const DrtPass p, const __grid_constant__ CUtensorMap zmap)
             }
 #endif
         }
-#pragma unroll
-        for (int k = 0; k < NCK; ++k) {
-            uint32_t v[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) v[i] = __byte_perm(w[4 * k + i], w[4 * k + i + 1], sel);
+#ifndef D3_SWAR_ST256
+#define D3_SWAR_ST256 1      // measured: cfg3 first pass 0.452 -> 0.392 ms (the L1 data pipe is its limiter)
+#endif
+        auto store_chunk = [&](int k, const uint32_t (&v)[4]) {
             if (d0 + 8 * k < p.out_width) {
                 if (k == NCK - 1) store_chunk_head<2>(dst + 8 * k, v, 8 - rho);
 #ifdef D3_STAGE_EVICT_LAST
@@ -488,7 +487,38 @@ drt_first_swar_kernel(const DrtPass p, const __grid_constant__ CUtensorMap zmap)
                 else *reinterpret_cast<uint4 *>(dst + 8 * k) = make_uint4(v[0], v[1], v[2], v[3]);
 #endif
             }
+        };
+#if D3_SWAR_ST256
+        // chunk pairs (2j, 2j + 1) below the head chunk leave as one 32-byte store (STG.256: a whole
+        // sector per lane); al32 is uniform over the CTA
+        static_assert(NCK % 2 == 0, "chunk pairs");
+        const bool al32 = (p.out_pitch % 16 == 0) && (p.out_inst_stride % 16 == 0) &&
+                          ((reinterpret_cast<unsigned long long>(outp) & 31ull) == 0);
+#pragma unroll
+        for (int k = 0; k < NCK; k += 2) {
+            uint32_t va[4], vb[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                va[i] = __byte_perm(w[4 * k + i], w[4 * k + i + 1], sel);
+                vb[i] = __byte_perm(w[4 * k + 4 + i], w[4 * k + 5 + i], sel);
+            }
+            if (k + 1 < NCK - 1 && al32 && d0 + 8 * (k + 1) < p.out_width) {
+                const uint32_t v8[8] = {va[0], va[1], va[2], va[3], vb[0], vb[1], vb[2], vb[3]};
+                st_v8(dst + 8 * k, v8);
+            } else {
+                store_chunk(k, va);
+                store_chunk(k + 1, vb);
+            }
         }
+#else
+#pragma unroll
+        for (int k = 0; k < NCK; ++k) {
+            uint32_t v[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v[i] = __byte_perm(w[4 * k + i], w[4 * k + i + 1], sel);
+            store_chunk(k, v);
+        }
+#endif
         if (rho > 0 && d0 >= 8) {
             // tile elements [0, rho) end the previous chunk: window (zeros, row words 0..3)
             const uint32_t *r0 = reinterpret_cast<const uint32_t *>(sm + G::ORP * rr) + row_skew<S>(r1);

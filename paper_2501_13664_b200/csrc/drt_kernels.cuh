@@ -1044,6 +1044,20 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
                         *reinterpret_cast<uint4 *>(dst + 8 * q) = make_uint4(w[0], w[1], w[2], w[3]);
                     }
                 } else {
+#ifndef D3_DRT_ST256
+#define D3_DRT_ST256 0
+#endif
+                    if constexpr (D3_DRT_ST256 && R == 8) {
+                        // an 8-element run of a 32-byte-aligned row position: one STG.256
+                        if ((reinterpret_cast<unsigned long long>(dst) & 31ull) == 0) {
+                            uint32_t v[8];
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) v[j] = Lane<Acc>::bits(acc[r2][j]);
+                            if (FINAL) st_cs_v8(dst, v);
+                            else st_v8(dst, v);
+                            continue;
+                        }
+                    }
 #pragma unroll
                     for (int q = 0; q < R / 4; ++q) {
                         const uint32_t a0 = Lane<Acc>::bits(acc[r2][4 * q + 0]), a1 = Lane<Acc>::bits(acc[r2][4 * q + 1]);

@@ -288,6 +288,27 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(THREADS, 2) drt_sep
             if (D3_SEP_ABL & 1) {
                 if (Lane<Acc>::bits(acc[0][0]) == 0x7f7f7f7fu) orow[0] = acc[3][11];   // keep the sums live
             } else if (!skip) {
+#ifndef D3_SEP_ST256
+#define D3_SEP_ST256 0
+#endif
+#if D3_SEP_ST256
+                // a 48-byte run = one 32-byte store (STG.256) + one 16-byte store; runs start 32-byte
+                // aligned on even lanes and 16 bytes past on odd ones (rows are 384 bytes)
+                if ((reinterpret_cast<unsigned long long>(outp) & 31ull) == 0) {
+                    const bool odd = run & 1;
+#pragma unroll
+                    for (int rho = 0; rho < 4; ++rho) {
+                        uint32_t v8[8], v4[4];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) v8[j] = odd ? Lane<Acc>::bits(acc[rho][4 + j]) : Lane<Acc>::bits(acc[rho][j]);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) v4[j] = odd ? Lane<Acc>::bits(acc[rho][j]) : Lane<Acc>::bits(acc[rho][8 + j]);
+                        Acc *o = orow + rho * (3 * N);
+                        st_cs_v8(o + (odd ? 4 : 0), v8);
+                        st_cs_v4(o + (odd ? 0 : 8), v4[0], v4[1], v4[2], v4[3]);
+                    }
+                } else
+#endif
 #pragma unroll
                 for (int rho = 0; rho < 4; ++rho)
 #pragma unroll
