@@ -110,9 +110,25 @@ template <int S> __device__ __forceinline__ int copy_row(int i) {
 #define SWAR_FMA16 0                                      // all adds IADD3 (measured fastest)
 #endif
 
+// TMA staging of the cube brick (D3_SWAR_TMA_STAGE, K = 4, N >= 128).  The first pass is limited by
+// the L1 data pipe, and a fifth of its wavefronts were the scattered 16-byte cube loads (every lane
+// a different line).  Instead one TMA tensor load brings the tile's 16 x 16 x BW voxel brick of the
+// ORIGINAL cube into shared memory (zero-filled outside the cube), the threads read it into
+// registers with LDS.128 and, after a barrier, pack over it.  Three maps of cube[batch][x][y][z],
+// one per original axis a that z' runs along: a = 2 (z' along z): box {BW, 16, 16} over (z, y, x);
+// a = 0 / 1: box {16, 16, BW} over (z, y, x) / (z, x, y), i.e. the BW-long side outermost, so the
+// 16-byte vectors of one z' are contiguous.
+struct SwarCubeMaps {
+    CUtensorMap m[3];
+};
+#ifndef D3_SWAR_TMA_STAGE
+#define D3_SWAR_TMA_STAGE 1
+#endif
+
 template <int K, int R, int T>
 __global__ void __launch_bounds__(SwarGeom<K, R, T>::THREADS) __maxnreg__((SwarGeom<K, R, T>::MAXREG))
-drt_first_swar_kernel(const DrtPass p, const __grid_constant__ CUtensorMap zmap) {
+drt_first_swar_kernel(const DrtPass p, const __grid_constant__ CUtensorMap zmap, const __grid_constant__ SwarCubeMaps cmap,
+                      const int tma_in) {
     using G = SwarGeom<K, R, T>;
     constexpr int S = G::S, H2 = G::H2, SP = G::SP, BW = G::BW;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -152,7 +168,182 @@ drt_first_swar_kernel(const DrtPass p, const __grid_constant__ CUtensorMap zmap)
         auto vox = [&](int x, int y, int z) -> const uint8_t * {
             return cube + o.off0 + (long long)x * o.sx + (long long)y * o.sy + (long long)z * o.sz;
         };
-        if (K == 4 && p.vec_ok && o.fast == 2 && (z0 & 15) == 0) {
+        if (K == 4 && D3_SWAR_TMA_STAGE && tma_in && (z0 & 15) == 0 && (o.fast != 2 || o.sz == 1)) {
+            if constexpr (K == 4) {
+            // ---- brick by TMA, packed from shared memory (see SwarCubeMaps)
+            uint64_t *bar = reinterpret_cast<uint64_t *>(sm + G::SMEM);
+            const long long sv[3] = {o.sx, o.sy, o.sz};
+            const int lo[3] = {xb, yb, z0}, ext[3] = {S, S, BW};
+            int aj[3], start[3];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const long long a = sv[j] < 0 ? -sv[j] : sv[j];
+                aj[j] = a == 1 ? 2 : (a == (long long)N ? 1 : 0);       // original axis of oriented axis j
+            }
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+                    if (aj[j] == a) start[a] = sv[j] > 0 ? lo[j] : N - lo[j] - ext[j];
+            // dense brick, byte multiplier of each oriented axis (see SwarCubeMaps)
+            const int kind = aj[2], other = 1 - kind;         // kind != 2: the 16-long non-inner original axis
+            int ss[3], soff = 0;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const int mm = kind == 2 ? (aj[j] == 2 ? 1 : (aj[j] == 1 ? BW : S * BW))
+                                         : (aj[j] == 2 ? 1 : (j == 2 ? S * S : S));
+                ss[j] = sv[j] > 0 ? mm : -mm;
+                if (sv[j] < 0) soff += (ext[j] - 1) * mm;
+            }
+            const int c1 = kind == 2 ? start[1] : (other == 1 ? start[1] : start[0]);
+            const int c2 = kind == 2 ? start[0] : start[kind == 0 ? 0 : 1];
+            const uint32_t smb = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+            const uint32_t barb = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+            if (tid == 0) {
+                asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(barb), "r"(1) : "memory");
+                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(barb), "r"(S * S * BW) : "memory");
+                asm volatile(
+                    "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smb),
+                    "l"(&cmap.m[kind]), "r"(start[2]), "r"(c1), "r"(c2), "r"(inst / p.ndod), "r"(barb)
+                    : "memory");
+            }
+            __syncthreads();                                  // the barrier is initialised
+            asm volatile(
+                "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}" ::"r"(barb)
+                : "memory");
+            // 16-byte vector at brick offset `off` (a multiple of 16)
+            auto lds16 = [&](int off) -> uint4 {
+                uint4 v;
+                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                             : "r"(smb + (uint32_t)off));
+                return v;
+            };
+            // Lane orders below keep a quarter-warp's 8 brick vectors AND its 8 packed chunks in
+            // distinct 16-byte bank groups: the brick group depends on the 16-long axis index, the
+            // packed group on (pw + chunk) mod 8 (slots are 25 chunks apart), hence the diagonals.
+            if (o.fast == 2) {
+                // z' contiguous: rows pw and pw + 8 of slot (w1, pw), 16 voxels = 4 packed chunks.
+                // When x' runs along the brick's outer side (y), w1 advances with pw (rows 96 bytes apart)
+                constexpr int NQ = BW / 16, NIT = (G::NSLOT * NQ + G::THREADS - 1) / G::THREADS;
+                const bool diag = (ss[0] < 0 ? -ss[0] : ss[0]) < (ss[1] < 0 ? -ss[1] : ss[1]);
+                uint4 a[NIT], b[NIT];
+#pragma unroll
+                for (int u = 0; u < NIT; ++u) {
+                    const int it = tid + u * G::THREADS;
+                    const int sl = it & (G::NSLOT - 1), q = it / G::NSLOT;
+                    const int pw = sl & (H2 - 1), w1 = ((sl / H2) + (diag ? pw : 0)) & (S - 1);
+                    a[u] = make_uint4(0u, 0u, 0u, 0u);
+                    b[u] = a[u];
+                    if (it < G::NSLOT * NQ) {
+                        const int off = soff + w1 * ss[0] + pw * ss[1] + 16 * q;
+                        a[u] = lds16(off);
+                        b[u] = lds16(off + H2 * ss[1]);
+                    }
+                }
+                __syncthreads();                              // the brick is in registers: pack over it
+#pragma unroll
+                for (int u = 0; u < NIT; ++u) {
+                    const int it = tid + u * G::THREADS;
+                    if (it < G::NSLOT * NQ) {
+                        const int sl = it & (G::NSLOT - 1), q = it / G::NSLOT;
+                        const int pw = sl & (H2 - 1), w1 = ((sl / H2) + (diag ? pw : 0)) & (S - 1);
+                        const uint32_t av[4] = {a[u].x, a[u].y, a[u].z, a[u].w}, bv[4] = {b[u].x, b[u].y, b[u].z, b[u].w};
+#pragma unroll
+                        for (int h = 0; h < 4; ++h) {
+                            uint32_t w[4];
+                            pair_bytes(av[h], bv[h], w);
+                            put4(w1 * H2 + pw, 4 * q + h, w[0], w[1], w[2], w[3]);
+                        }
+                    }
+                }
+            } else if (o.fast == 1) {
+                // y' contiguous: one vector = all 16 w2 of (w1, z'); item (w1, e4) = 4 consecutive z',
+                // lanes along w1 with e4 on the diagonal
+                const bool fwd = ss[1] > 0;
+                const int yoff = soff + (fwd ? 0 : 15 * ss[1]);
+                constexpr int NE4 = BW / 4, NI = (S * NE4 + G::THREADS - 1) / G::THREADS;
+                uint4 v[NI][4];
+#pragma unroll
+                for (int u = 0; u < NI; ++u) {
+                    const int it = tid + u * G::THREADS;
+                    const int w1 = it & (S - 1), e4 = ((it / S) + w1) % NE4;
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        v[u][t] = make_uint4(0u, 0u, 0u, 0u);
+                        if (it < S * NE4) v[u][t] = lds16(yoff + w1 * ss[0] + (4 * e4 + t) * ss[2]);
+                    }
+                }
+                __syncthreads();
+#pragma unroll
+                for (int u = 0; u < NI; ++u) {
+                    const int it = tid + u * G::THREADS;
+                    if (it >= S * NE4) break;
+                    const int w1 = it & (S - 1), e4 = ((it / S) + w1) % NE4;
+                    uint32_t wd[4][H2];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const uint4 x = fwd ? v[u][t] : rev16(v[u][t]);   // byte b <-> w2 = b
+                        uint32_t l4[4], h4[4];
+                        pair_bytes(x.x, x.z, l4);          // w2 = 0..3 with 8..11
+                        pair_bytes(x.y, x.w, h4);          // w2 = 4..7 with 12..15
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            wd[t][j] = l4[j];
+                            wd[t][4 + j] = h4[j];
+                        }
+                    }
+#pragma unroll
+                    for (int pw = 0; pw < H2; ++pw) put4(w1 * H2 + pw, e4, wd[0][pw], wd[1][pw], wd[2][pw], wd[3][pw]);
+                }
+            } else {
+                // x' contiguous: one vector = all 16 w1 of (w2, z'); item (pw, e4): rows pw and pw + 8,
+                // lanes along pw with e4 on the diagonal (step 2: (pw + chunk) mod 8 = 3 pw + const)
+                const bool fwd = ss[0] > 0;
+                const int xoff = soff + (fwd ? 0 : 15 * ss[0]);
+                constexpr int NE4 = BW / 4, NI = (H2 * NE4 + G::THREADS - 1) / G::THREADS;
+                uint4 a[NI][4], b[NI][4];
+#pragma unroll
+                for (int u = 0; u < NI; ++u) {
+                    const int it = tid + u * G::THREADS;
+                    const int pw = it & (H2 - 1), e4 = ((it / H2) + 2 * pw) % NE4;
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        a[u][t] = make_uint4(0u, 0u, 0u, 0u);
+                        b[u][t] = a[u][t];
+                        if (it < H2 * NE4) {
+                            const int off = xoff + pw * ss[1] + (4 * e4 + t) * ss[2];
+                            a[u][t] = lds16(off);
+                            b[u][t] = lds16(off + H2 * ss[1]);
+                        }
+                    }
+                }
+                __syncthreads();
+#pragma unroll
+                for (int u = 0; u < NI; ++u) {
+                    const int it = tid + u * G::THREADS;
+                    if (it >= H2 * NE4) break;
+                    const int pw = it & (H2 - 1), e4 = ((it / H2) + 2 * pw) % NE4;
+                    uint32_t wd[4][S];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const uint4 xa = fwd ? a[u][t] : rev16(a[u][t]), xb4 = fwd ? b[u][t] : rev16(b[u][t]);
+                        const uint32_t av[4] = {xa.x, xa.y, xa.z, xa.w}, bv[4] = {xb4.x, xb4.y, xb4.z, xb4.w};
+#pragma unroll
+                        for (int h = 0; h < 4; ++h) {
+                            uint32_t w[4];
+                            pair_bytes(av[h], bv[h], w);
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) wd[t][4 * h + j] = w[j];
+                        }
+                    }
+#pragma unroll
+                    for (int w1 = 0; w1 < S; ++w1) put4(w1 * H2 + pw, e4, wd[0][w1], wd[1][w1], wd[2][w1], wd[3][w1]);
+                }
+            }
+            }
+        } else if (K == 4 && p.vec_ok && o.fast == 2 && (z0 & 15) == 0) {
             // z' contiguous (forward): two LDG.128 (rows pw, pw + 8) -> 16 packed words.  Item
             // it = slot + NSLOT * q (consecutive lanes: consecutive slots, conflict-free STS); all of
             // a thread's loads are issued before any is consumed so their L2 latencies overlap.

@@ -86,7 +86,7 @@ drt3d_status launch_drt_k(const DrtPass &prm_in, int ninst, cudaStream_t st) {
             using SG = SwarGeom<K, RR, TT>;
             auto kern = drt_first_swar_kernel<K, RR, TT>;
             static std::atomic<uint32_t> smem_done{0};
-            if (!set_smem_once(kern, SG::SMEM, smem_done)) return DRT3D_ERR_CUDA;
+            if (!set_smem_once(kern, SG::SMEM + 16, smem_done)) return DRT3D_ERR_CUDA;      // + the staging mbarrier
             const int ntiles = (prm.out_width + 8 + TT - 1) / TT;
             dim3 grid(ntiles, (unsigned)groups, ninst);
             // the final pass's zero tiles (api.cu, DESIGN.md §5 item 6): map of the final output
@@ -96,7 +96,28 @@ drt3d_status launch_drt_k(const DrtPass &prm_in, int ninst, cudaStream_t st) {
             if (q.zf_T > 0 && !(K == 4 && q.zf_T == D3_FINAL16_T && SG::SMEM >= (1 << (2 * K)) * D3_FINAL16_T * 4 &&
                                 make_out_map(&zmap, q.zf_out, q.N, q.inst_total, q.zf_T, 1 << K, 1 << K)))
                 return DRT3D_ERR_UNSUPPORTED;
-            kern<<<grid, SG::THREADS, SG::SMEM, st>>>(q, zmap);
+            // cube brick maps for the TMA staging (drt_first_swar.cuh, SwarCubeMaps): cube[batch][x][y][z]
+            // u8, box BW along original axis a and 16 along the other two; boxes must fit the cube
+            SwarCubeMaps cm;
+            std::memset(&cm, 0, sizeof(cm));
+            int tma_in = 0;
+            if (K == 4 && D3_SWAR_TMA_STAGE && q.N >= 128 && q.vec_ok) {
+                auto enc = tmap_encoder();
+                const cuuint64_t Nn = (cuuint64_t)q.N, nb = (cuuint64_t)((q.inst_total + q.ndod - 1) / q.ndod);
+                cuuint64_t dims[4] = {Nn, Nn, Nn, nb};
+                cuuint32_t es[4] = {1, 1, 1, 1};
+                tma_in = enc != nullptr;
+                for (int a = 0; a < 3 && tma_in; ++a) {
+                    // a = 1: dimensions (z, x, y), so that the BW-long side is outermost
+                    cuuint64_t str[3] = {a == 1 ? Nn * Nn : Nn, a == 1 ? Nn : Nn * Nn, Nn * Nn * Nn};
+                    cuuint32_t box[4] = {16, 16, 16, 1};
+                    box[a == 2 ? 0 : 2] = (cuuint32_t)SG::BW;
+                    tma_in = enc(&cm.m[a], CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void *>(q.in), dims, str, box, es,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+                }
+            }
+            kern<<<grid, SG::THREADS, SG::SMEM + 16, st>>>(q, zmap, cm, tma_in);
             return DRT3D_OK;
         };
         if constexpr (K == 4 && T == 64) {
