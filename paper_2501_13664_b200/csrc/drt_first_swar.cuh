@@ -120,6 +120,7 @@ template <int S> __device__ __forceinline__ int copy_row(int i) {
 // 16-byte vectors of one z' are contiguous.
 struct SwarCubeMaps {
     CUtensorMap m[3];
+    CUtensorMap st;       // the stage-K rows this pass writes (D3_SWAR_TMA_OUT, the copy-out)
 };
 #ifndef D3_SWAR_TMA_STAGE
 #define D3_SWAR_TMA_STAGE 1
@@ -128,7 +129,7 @@ struct SwarCubeMaps {
 template <int K, int R, int T>
 __global__ void __launch_bounds__(SwarGeom<K, R, T>::THREADS) __maxnreg__((SwarGeom<K, R, T>::MAXREG))
 drt_first_swar_kernel(const DrtPass p, const __grid_constant__ CUtensorMap zmap, const __grid_constant__ SwarCubeMaps cmap,
-                      const int tma_in) {
+                      const int tma_in, const int tma_out) {
     using G = SwarGeom<K, R, T>;
     constexpr int S = G::S, H2 = G::H2, SP = G::SP, BW = G::BW;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -633,6 +634,81 @@ drt_first_swar_kernel(const DrtPass p, const __grid_constant__ CUtensorMap zmap,
         }
     }
 #else
+#ifndef D3_SWAR_TMA_OUT
+#define D3_SWAR_TMA_OUT 0     // measured (bit-exact): cfg3 first pass 0.365 ms vs 0.331 with the LSU copy-out
+#endif
+#ifndef D3_SWAR_TMA_OUT_FULLWAIT
+#define D3_SWAR_TMA_OUT_FULLWAIT 1
+#endif
+    if (K == 4 && D3_SWAR_TMA_OUT && tma_out) {
+        // Chunks 0 .. NCK - 2 of every row (whole for any rho) leave with ONE TMA tensor store of a
+        // dense 256-row image (smap: stage rows as [inst][r1 r2][V1 V2][D], box {8 (NCK - 1), 1, 256, 1});
+        // only the last chunk (head) and the tail before the tile stay on the LSU (the L1 data pipe
+        // is this pass's limiter).  The image is written over the unpacked rows, so every thread first
+        // reads and shifts its rows into registers.
+        constexpr int NRW = (S * S + G::THREADS - 1) / G::THREADS, IMGP = (NCK - 1) * 16;
+        uint32_t w[NRW][4 * NCK + 1], tw4[NRW][4];
+#pragma unroll
+        for (int u = 0; u < NRW; ++u) {
+            const int ii = tid + u * G::THREADS;
+            if (ii < S * S) {
+                const int rr = copy_row<S>(ii), r1 = rr >> K, r2 = rr & (S - 1);
+                const int rho = (r1 * wv1 + r2 * wv2) & 7;
+                const uint32_t *srow = reinterpret_cast<const uint32_t *>(sm + G::ORP * rr) + row_skew<S>(r1);
+                uint32_t w0[4 * NCK + 4];
+#pragma unroll
+                for (int i = 0; i < 4 * NCK + 4; ++i) w0[i] = srow[i];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) tw4[u][i] = w0[i];
+                const int q = rho >> 1;
+                const bool b0 = q & 1, b1 = (q & 2) != 0;
+#pragma unroll
+                for (int i = 0; i < 4 * NCK + 3; ++i) w0[i] = b0 ? w0[i + 1] : w0[i];
+#pragma unroll
+                for (int i = 0; i < 4 * NCK + 1; ++i) w[u][i] = b1 ? w0[i + 2] : w0[i];
+            }
+        }
+        __syncthreads();                                      // every unpacked row is in registers
+#pragma unroll
+        for (int u = 0; u < NRW; ++u) {
+            const int ii = tid + u * G::THREADS;
+            if (ii < S * S) {
+                const int rr = copy_row<S>(ii), r1 = rr >> K, r2 = rr & (S - 1);
+                const int rho = (r1 * wv1 + r2 * wv2) & 7;
+                const uint32_t sel = (rho & 1) ? 0x5432u : 0x3210u;
+#pragma unroll
+                for (int k = 0; k < NCK - 1; ++k)
+                    *reinterpret_cast<uint4 *>(sm + rr * IMGP + 16 * k) =
+                        make_uint4(__byte_perm(w[u][4 * k], w[u][4 * k + 1], sel), __byte_perm(w[u][4 * k + 1], w[u][4 * k + 2], sel),
+                                   __byte_perm(w[u][4 * k + 2], w[u][4 * k + 3], sel), __byte_perm(w[u][4 * k + 3], w[u][4 * k + 4], sel));
+                const long long row = ((((long long)r1 << K) + r2) << (2 * m)) + ((long long)V1 << m) + V2;
+                uint16_t *dst = outp + out_inst + row * p.out_pitch + d0;
+                if (d0 + 8 * (NCK - 1) < p.out_width) {
+                    constexpr int k = NCK - 1;
+                    uint32_t v[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) v[i] = __byte_perm(w[u][4 * k + i], w[u][4 * k + i + 1], sel);
+                    store_chunk_head<2>(dst + 8 * k, v, 8 - rho);
+                }
+                if (rho > 0 && d0 >= 8) {
+                    const uint32_t tw[8] = {0u, 0u, 0u, 0u, tw4[u][0], tw4[u][1], tw4[u][2], tw4[u][3]};
+                    uint32_t v[4];
+                    window_chunk<2>(tw, rho, 0, v);
+                    store_chunk_tail<2>(dst - 8, v, rho);
+                }
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (tid == 0 && d0 < p.out_width) {
+            asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(&cmap.st),
+                         "r"(d0), "r"((V1 << m) + V2), "r"(0), "r"(li), "r"(static_cast<uint32_t>(__cvta_generic_to_shared(sm)))
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            if (D3_SWAR_TMA_OUT_FULLWAIT) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+            else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+    } else
     for (int ii = tid; ii < S * S; ii += blockDim.x) {
         const int rr = copy_row<S>(ii);
         const int r1 = rr >> K, r2 = rr & (S - 1);

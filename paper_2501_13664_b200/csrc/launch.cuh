@@ -101,7 +101,10 @@ drt3d_status launch_drt_k(const DrtPass &prm_in, int ninst, cudaStream_t st) {
             SwarCubeMaps cm;
             std::memset(&cm, 0, sizeof(cm));
             int tma_in = 0;
-            if (K == 4 && D3_SWAR_TMA_STAGE && q.N >= 128 && q.vec_ok) {
+            #ifndef D3_SWAR_TMA_MIN_N
+#define D3_SWAR_TMA_MIN_N 128
+#endif
+            if (K == 4 && D3_SWAR_TMA_STAGE && q.N >= D3_SWAR_TMA_MIN_N && q.vec_ok) {
                 auto enc = tmap_encoder();
                 const cuuint64_t Nn = (cuuint64_t)q.N, nb = (cuuint64_t)((q.inst_total + q.ndod - 1) / q.ndod);
                 cuuint64_t dims[4] = {Nn, Nn, Nn, nb};
@@ -117,7 +120,22 @@ drt3d_status launch_drt_k(const DrtPass &prm_in, int ninst, cudaStream_t st) {
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
                 }
             }
-            kern<<<grid, SG::THREADS, SG::SMEM + 16, st>>>(q, zmap, cm, tma_in);
+            // stage-K rows as [inst][r1 r2][V1 V2][D] (u16): the copy-out's whole chunks of a tile's
+            // 256 rows leave with one TMA store
+            int tma_out = 0;
+            if (K == 4 && D3_SWAR_TMA_OUT) {
+                auto enc = tmap_encoder();
+                const cuuint64_t pb = (cuuint64_t)q.out_pitch * 2;
+                cuuint64_t dims[4] = {(cuuint64_t)q.out_width, (cuuint64_t)groups, 1ull << (2 * K), (cuuint64_t)ninst};
+                cuuint64_t str[3] = {pb, pb * groups, (cuuint64_t)q.out_inst_stride * 2};
+                cuuint32_t box[4] = {(cuuint32_t)(TT - 8), 1, 1u << (2 * K), 1}, es[4] = {1, 1, 1, 1};
+                tma_out = enc != nullptr && (reinterpret_cast<uintptr_t>(q.out) & 15) == 0 && pb % 16 == 0 &&
+                          (q.out_inst_stride * 2) % 16 == 0 &&
+                          enc(&cm.st, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, q.out, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+            }
+            kern<<<grid, SG::THREADS, SG::SMEM + 16, st>>>(q, zmap, cm, tma_in, tma_out);
             return DRT3D_OK;
         };
         if constexpr (K == 4 && T == 64) {
