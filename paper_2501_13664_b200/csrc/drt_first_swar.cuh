@@ -19,16 +19,25 @@
 
 namespace d3 {
 
-template <int K, int R, int T>
+// E > 0 (the TMA-staged K = 4 kernel): a tile computes TE = T + E outputs per row but still owns the
+// T stored positions [d0, d0 + T).  Rows are stored shifted left by rho <= 7, so with E = 8 every one
+// of the tile's T / 8 stored chunks is whole (elements [d0 + rho, d0 + T + rho) are all computed
+// here): the copy-out has no partial head / tail stores, which were 3 of its 7 store instructions
+// per row on the L1 data pipe that limits this pass.  The extra run per row is taken by threads
+// that were idle (x-step 88 of 96, y-step 72 of 96 at T = 64).
+template <int K, int R, int T, int E = 0>
 struct SwarGeom {
     static constexpr int S = 1 << K;
     static constexpr int H2 = S / 2;                      // lane pairing distance
     static constexpr int H = S - 1;
-    static constexpr int WIN = T + 2 * H;
-    static constexpr int NRX = (T + H + R - 1) / R;
-    static constexpr int NRY = T / R;
+    static constexpr int TE = T + E;                      // outputs computed per row
+    static constexpr int WIN = TE + 2 * H;
+    static constexpr int NRX = (TE + H + R - 1) / R;
+    static constexpr int NRY = TE / R;
     static constexpr int RD = (NRX - 1) * R + (R + H + 3) / 4 * 4;
-    static constexpr int BW = ((WIN > RD ? WIN : RD) + 15) / 16 * 16;   // staged words per slot
+    static constexpr int BWG = E > 0 ? 8 : 16;            // E > 0 keeps the slots small enough for 4 CTAs per SM
+    static constexpr int BW = ((WIN > RD ? WIN : RD) + BWG - 1) / BWG * BWG;   // staged words per slot
+    static constexpr int BWI = (BW + 15) / 16 * 16;       // brick extent along a contiguous z' (whole 16-byte vectors)
     static constexpr int XB = NRX * R * 4;
     static constexpr int SP0 = (BW * 4 > XB ? BW * 4 : XB);
     static constexpr int SP = SP0 + 16;                   // slot pitch (bytes); +16 rotates banks
@@ -36,7 +45,7 @@ struct SwarGeom {
     static constexpr int XT = H2 * NRX;                   // x-step tasks
     static constexpr int YT = H2 * NRY;                   // y-step tasks
     static constexpr int THREADS = ((XT > YT ? XT : YT) + 31) / 32 * 32;
-    static constexpr int ORW = T / 2;                     // output staging: words per row
+    static constexpr int ORW = TE / 2;                    // output staging: words per row
     static constexpr int ORP = (ORW + 1) * 4;             // odd word pitch: rows hit distinct banks
     static constexpr int SMEM0 = NSLOT * SP;
     static constexpr int SMEM = (SMEM0 > S * S * ORP ? SMEM0 : S * S * ORP);
@@ -50,8 +59,9 @@ struct SwarGeom {
     static constexpr int CTAS = K == 4 ? SWAR_CTAS : SWAR_CTAS3;
     static constexpr int MAXREG0 = 65536 / (CTAS * THREADS) / 8 * 8;
     static constexpr int MAXREG = MAXREG0 > 255 ? 255 : MAXREG0;
-    static_assert(T % R == 0 && (R == 8 || R == 4), "tile shape");
-    static_assert(NRY == 8 || NRY == 16, "y runs per row must be a shuffle width");
+    static_assert(T % R == 0 && E % R == 0 && (R == 8 || R == 4), "tile shape");
+    static_assert(NRY == 8 || NRY == 16 || E > 0, "y runs per row must be a shuffle width");
+    static_assert(S * S * BWI <= SMEM0, "the cube brick fits the slots");
 };
 
 // word = lo | hi << 16 for the four byte pairs (a.b_i, b.b_i): 6 PRMT per 4 words
@@ -126,12 +136,13 @@ struct SwarCubeMaps {
 #define D3_SWAR_TMA_STAGE 1
 #endif
 
-template <int K, int R, int T>
-__global__ void __launch_bounds__(SwarGeom<K, R, T>::THREADS) __maxnreg__((SwarGeom<K, R, T>::MAXREG))
+template <int K, int R, int T, int E = 0>
+__global__ void __launch_bounds__(SwarGeom<K, R, T, E>::THREADS) __maxnreg__((SwarGeom<K, R, T, E>::MAXREG))
 drt_first_swar_kernel(const DrtPass p, const __grid_constant__ CUtensorMap zmap, const __grid_constant__ SwarCubeMaps cmap,
                       const int tma_in, const int tma_out) {
-    using G = SwarGeom<K, R, T>;
+    using G = SwarGeom<K, R, T, E>;
     constexpr int S = G::S, H2 = G::H2, SP = G::SP, BW = G::BW;
+    static_assert(E == 0 || (K == 4 && E == 8), "E = 8: the TMA-staged K = 4 kernel");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     unsigned char *sm = smem_raw;
 
@@ -169,6 +180,7 @@ drt_first_swar_kernel(const DrtPass p, const __grid_constant__ CUtensorMap zmap,
         auto vox = [&](int x, int y, int z) -> const uint8_t * {
             return cube + o.off0 + (long long)x * o.sx + (long long)y * o.sy + (long long)z * o.sz;
         };
+        if (E > 0 && !(tma_in && (z0 & 15) == 0 && (o.fast != 2 || o.sz == 1))) __trap();   // host: E > 0 only with the brick load
         if (K == 4 && D3_SWAR_TMA_STAGE && tma_in && (z0 & 15) == 0 && (o.fast != 2 || o.sz == 1)) {
             if constexpr (K == 4) {
             // ---- brick by TMA, packed from shared memory (see SwarCubeMaps)
@@ -191,7 +203,7 @@ drt_first_swar_kernel(const DrtPass p, const __grid_constant__ CUtensorMap zmap,
             int ss[3], soff = 0;
 #pragma unroll
             for (int j = 0; j < 3; ++j) {
-                const int mm = kind == 2 ? (aj[j] == 2 ? 1 : (aj[j] == 1 ? BW : S * BW))
+                const int mm = kind == 2 ? (aj[j] == 2 ? 1 : (aj[j] == 1 ? G::BWI : S * G::BWI))
                                          : (aj[j] == 2 ? 1 : (j == 2 ? S * S : S));
                 ss[j] = sv[j] > 0 ? mm : -mm;
                 if (sv[j] < 0) soff += (ext[j] - 1) * mm;
@@ -203,7 +215,7 @@ drt_first_swar_kernel(const DrtPass p, const __grid_constant__ CUtensorMap zmap,
             if (tid == 0) {
                 asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(barb), "r"(1) : "memory");
                 asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(barb), "r"(S * S * BW) : "memory");
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(barb), "r"(S * S * (kind == 2 ? G::BWI : BW)) : "memory");
                 asm volatile(
                     "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smb),
                     "l"(&cmap.m[kind]), "r"(start[2]), "r"(c1), "r"(c2), "r"(inst / p.ndod), "r"(barb)
@@ -227,7 +239,7 @@ drt_first_swar_kernel(const DrtPass p, const __grid_constant__ CUtensorMap zmap,
             if (o.fast == 2) {
                 // z' contiguous: rows pw and pw + 8 of slot (w1, pw), 16 voxels = 4 packed chunks.
                 // When x' runs along the brick's outer side (y), w1 advances with pw (rows 96 bytes apart)
-                constexpr int NQ = BW / 16, NIT = (G::NSLOT * NQ + G::THREADS - 1) / G::THREADS;
+                constexpr int NQ = G::BWI / 16, NIT = (G::NSLOT * NQ + G::THREADS - 1) / G::THREADS;
                 const bool diag = (ss[0] < 0 ? -ss[0] : ss[0]) < (ss[1] < 0 ? -ss[1] : ss[1]);
                 uint4 a[NIT], b[NIT];
 #pragma unroll
@@ -255,7 +267,7 @@ drt_first_swar_kernel(const DrtPass p, const __grid_constant__ CUtensorMap zmap,
                         for (int h = 0; h < 4; ++h) {
                             uint32_t w[4];
                             pair_bytes(av[h], bv[h], w);
-                            put4(w1 * H2 + pw, 4 * q + h, w[0], w[1], w[2], w[3]);
+                            if (G::BWI == BW || 4 * q + h < BW / 4) put4(w1 * H2 + pw, 4 * q + h, w[0], w[1], w[2], w[3]);
                         }
                     }
                 }
@@ -599,6 +611,7 @@ drt_first_swar_kernel(const DrtPass p, const __grid_constant__ CUtensorMap zmap,
 #define D3_SWAR_COPY_CHUNK 0              // measured: first pass 0.4575 ms vs 0.4514 with one row per thread
 #endif
 #if D3_SWAR_COPY_CHUNK
+    static_assert(E == 0, "chunk copy-out: E = 0 only");
     // one 16-byte chunk per item, 8 consecutive lanes per row: every store instruction of a warp
     // writes 4 whole 128-byte row segments; a lane reads its chunk's 5 words at the rho/2 word offset
     // (no select network) and the k = 0 lane also writes the tail chunk before the tile
@@ -640,7 +653,44 @@ drt_first_swar_kernel(const DrtPass p, const __grid_constant__ CUtensorMap zmap,
 #ifndef D3_SWAR_TMA_OUT_FULLWAIT
 #define D3_SWAR_TMA_OUT_FULLWAIT 1
 #endif
-    if (K == 4 && D3_SWAR_TMA_OUT && tma_out) {
+    if constexpr (E > 0) {
+        // every stored chunk of the tile is whole (SwarGeom): 32-byte stores, no head / tail
+        static_assert(E == 8 && NCK % 2 == 0, "E covers the largest shift");
+        const bool al32 = (p.out_pitch % 16 == 0) && (p.out_inst_stride % 16 == 0) &&
+                          ((reinterpret_cast<unsigned long long>(outp) & 31ull) == 0);
+        for (int ii = tid; ii < S * S; ii += blockDim.x) {
+            const int rr = copy_row<S>(ii);
+            const int r1 = rr >> K, r2 = rr & (S - 1);
+            const int rho = (r1 * wv1 + r2 * wv2) & 7;
+            const long long row = ((((long long)r1 << K) + r2) << (2 * m)) + ((long long)V1 << m) + V2;
+            uint16_t *dst = outp + out_inst + row * p.out_pitch + d0;
+            const uint32_t sel = (rho & 1) ? 0x5432u : 0x3210u;
+            const uint32_t *srow = reinterpret_cast<const uint32_t *>(sm + G::ORP * rr) + row_skew<S>(r1);
+            static_assert(G::ORW >= 4 * NCK + 4, "the row holds the shifted window");
+            uint32_t w0[4 * NCK + 4], w[4 * NCK + 1];
+#pragma unroll
+            for (int i = 0; i < 4 * NCK + 4; ++i) w0[i] = srow[i];
+            const int q = rho >> 1;
+            const bool b0 = q & 1, b1 = (q & 2) != 0;
+#pragma unroll
+            for (int i = 0; i < 4 * NCK + 3; ++i) w0[i] = b0 ? w0[i + 1] : w0[i];
+#pragma unroll
+            for (int i = 0; i < 4 * NCK + 1; ++i) w[i] = b1 ? w0[i + 2] : w0[i];
+#pragma unroll
+            for (int k = 0; k < NCK; k += 2) {
+                uint32_t v8[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v8[i] = __byte_perm(w[4 * k + i], w[4 * k + i + 1], sel);
+                if (al32 && d0 + 8 * (k + 1) < p.out_width) {
+                    st_v8(dst + 8 * k, v8);
+                } else {
+                    if (d0 + 8 * k < p.out_width) *reinterpret_cast<uint4 *>(dst + 8 * k) = make_uint4(v8[0], v8[1], v8[2], v8[3]);
+                    if (d0 + 8 * (k + 1) < p.out_width)
+                        *reinterpret_cast<uint4 *>(dst + 8 * (k + 1)) = make_uint4(v8[4], v8[5], v8[6], v8[7]);
+                }
+            }
+        }
+    } else if (K == 4 && D3_SWAR_TMA_OUT && tma_out) {
         // Chunks 0 .. NCK - 2 of every row (whole for any rho) leave with ONE TMA tensor store of a
         // dense 256-row image (smap: stage rows as [inst][r1 r2][V1 V2][D], box {8 (NCK - 1), 1, 256, 1});
         // only the last chunk (head) and the tail before the tile stay on the LSU (the L1 data pipe

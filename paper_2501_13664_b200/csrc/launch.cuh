@@ -9,7 +9,7 @@
 
 namespace d3 {
 
-template <int A, int B> struct IntPair { static constexpr int first = A, second = B; };
+template <int A, int B, int C = 0> struct IntPair { static constexpr int first = A, second = B, third = C; };
 
 // ---- DRT kernel selection
 template <int K> struct DrtTile;
@@ -78,13 +78,16 @@ drt3d_status launch_drt_k(const DrtPass &prm_in, int ninst, cudaStream_t st) {
 #ifndef D3_SWAR_SMALL_CTAS
 #define D3_SWAR_SMALL_CTAS 160
 #endif
+#ifndef D3_SWAR_TMA_MIN_N
+#define D3_SWAR_TMA_MIN_N 128           // N = 64 measured: no gain (cfg2 0.0317 vs 0.0297 ms)
+#endif
         const long long groups = 1LL << (2 * prm.m);
         const bool half = K == 4 && T == 64 && prm.zf_T == 0 &&
                           (long long)((prm.out_width + 8 + T - 1) / T) * groups * ninst < D3_SWAR_SMALL_CTAS;
         auto go = [&](auto geo) -> drt3d_status {
-            constexpr int RR = decltype(geo)::first, TT = decltype(geo)::second;
-            using SG = SwarGeom<K, RR, TT>;
-            auto kern = drt_first_swar_kernel<K, RR, TT>;
+            constexpr int RR = decltype(geo)::first, TT = decltype(geo)::second, EE = decltype(geo)::third;
+            using SG = SwarGeom<K, RR, TT, EE>;
+            auto kern = drt_first_swar_kernel<K, RR, TT, EE>;
             static std::atomic<uint32_t> smem_done{0};
             if (!set_smem_once(kern, SG::SMEM + 16, smem_done)) return DRT3D_ERR_CUDA;      // + the staging mbarrier
             const int ntiles = (prm.out_width + 8 + TT - 1) / TT;
@@ -101,9 +104,6 @@ drt3d_status launch_drt_k(const DrtPass &prm_in, int ninst, cudaStream_t st) {
             SwarCubeMaps cm;
             std::memset(&cm, 0, sizeof(cm));
             int tma_in = 0;
-            #ifndef D3_SWAR_TMA_MIN_N
-#define D3_SWAR_TMA_MIN_N 128
-#endif
             if (K == 4 && D3_SWAR_TMA_STAGE && q.N >= D3_SWAR_TMA_MIN_N && q.vec_ok) {
                 auto enc = tmap_encoder();
                 const cuuint64_t Nn = (cuuint64_t)q.N, nb = (cuuint64_t)((q.inst_total + q.ndod - 1) / q.ndod);
@@ -114,7 +114,7 @@ drt3d_status launch_drt_k(const DrtPass &prm_in, int ninst, cudaStream_t st) {
                     // a = 1: dimensions (z, x, y), so that the BW-long side is outermost
                     cuuint64_t str[3] = {a == 1 ? Nn * Nn : Nn, a == 1 ? Nn : Nn * Nn, Nn * Nn * Nn};
                     cuuint32_t box[4] = {16, 16, 16, 1};
-                    box[a == 2 ? 0 : 2] = (cuuint32_t)SG::BW;
+                    box[a == 2 ? 0 : 2] = (cuuint32_t)(a == 2 ? SG::BWI : SG::BW);
                     tma_in = enc(&cm.m[a], CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void *>(q.in), dims, str, box, es,
                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
@@ -135,11 +135,22 @@ drt3d_status launch_drt_k(const DrtPass &prm_in, int ninst, cudaStream_t st) {
                               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
             }
+            if (EE > 0 && !tma_in) return DRT3D_ERR_UNSUPPORTED;      // E > 0 needs the brick load: the caller falls back
             kern<<<grid, SG::THREADS, SG::SMEM + 16, st>>>(q, zmap, cm, tma_in, tma_out);
             return DRT3D_OK;
         };
         if constexpr (K == 4 && T == 64) {
             if (half) return go(IntPair<4, 32>{});
+#ifndef D3_SWAR_E8
+#define D3_SWAR_E8 0                    // measured (bit-exact): cfg3 first pass 0.3289 vs 0.3305 ms, N = 128 0.1341 vs 0.1321: neutral, off
+#endif
+            if constexpr (RS == 8 && D3_SWAR_E8 && D3_SWAR_TMA_STAGE) {
+                // the TMA-staged kernel with whole stored chunks (SwarGeom, E = 8)
+                if (prm.N >= D3_SWAR_TMA_MIN_N && prm.vec_ok) {
+                    const drt3d_status r = go(IntPair<RS, T, 8>{});
+                    if (r != DRT3D_ERR_UNSUPPORTED) return r;
+                }
+            }
         }
         return go(IntPair<RS, T>{});
     }

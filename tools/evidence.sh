@@ -16,4 +16,5 @@ timeout 900 ncu --set full --import-source on --clock-control none --cache-contr
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -shared -Xcompiler -fPIC tools/write_probe.cu -o tools/libwrite_probe.so > gpurun_out/ev_hbm_build_$TAG.log 2>&1
 timeout 300 python tools/hbm_write_probe.py > gpurun_out/ev_hbm_$TAG.log 2>&1; echo hbm=$? >> $S
 timeout 600 python tools/bench_configs.py > gpurun_out/ev_configs_$TAG.log 2>&1; echo configs=$? >> $S
+timeout 900 bash tools/ncu_configs.sh > gpurun_out/ncu_configs_$TAG.jsonl 2> gpurun_out/ev_ncucfg_$TAG.log; echo ncucfg=$? >> $S
 cat $S
