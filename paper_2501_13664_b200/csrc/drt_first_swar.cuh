@@ -221,10 +221,22 @@ drt_first_swar_kernel(const DrtPass p, const __grid_constant__ CUtensorMap zmap,
                     "l"(&cmap.m[kind]), "r"(start[2]), "r"(c1), "r"(c2), "r"(inst / p.ndod), "r"(barb)
                     : "memory");
             }
+#ifndef D3_SWAR_ONE_WAITER
+#define D3_SWAR_ONE_WAITER 0
+#endif
+            if (D3_SWAR_ONE_WAITER) {
+                // thread 0 alone waits for the brick, the CTA barrier then orders everyone after it
+                if (tid == 0)
+                    asm volatile(
+                        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}" ::"r"(barb)
+                        : "memory");
+                __syncthreads();
+            } else {
             __syncthreads();                                  // the barrier is initialised
             asm volatile(
                 "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}" ::"r"(barb)
                 : "memory");
+            }
             // 16-byte vector at brick offset `off` (a multiple of 16)
             auto lds16 = [&](int off) -> uint4 {
                 uint4 v;
