@@ -116,6 +116,16 @@ def test_drt_other_tables(N, table):
     assert np.array_equal(got.astype(np.int64), ref)
 
 
+@pytest.mark.parametrize("table", [d3.DRT3D_TABLE_PRINTED, d3.DRT3D_TABLE_SHARED])
+def test_drt_other_tables_n128_batched_full(table, tmp_path):
+    """N = 128 u8, two cubes, the PRINTED and SHARED tables, every element: the first pass's TMA
+    brick staging (DESIGN.md §5 item 9) over orientations the default table does not have (z' along
+    +x / +y, i.e. an unreversed long brick side off the contiguous axis) and over the batch
+    coordinate of its tensor maps."""
+    cube = synth.uniform_cube(128, 1280 + table, np.uint8, batch=2).reshape(2, 128, 128, 128)
+    _full_parity(tmp_path, cube, table=table, per_task=2)
+
+
 @pytest.mark.parametrize("mask", [0x001, 0x020, 0x210, 0x801, 0xAAA])
 def test_drt_masks(mask):
     cube = synth.uniform_cube(32, 300 + mask, np.uint8)
