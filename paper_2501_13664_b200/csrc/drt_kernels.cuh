@@ -790,6 +790,20 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
                 }
 #pragma unroll
                 for (int i = 0; i < 4; ++i) win[NWO + i] = __shfl_down_sync(0xffffffffu, win[i], 1, G::NRY);
+#ifndef D3_STAGE_ST256
+#define D3_STAGE_ST256 0          // measured slower: f32 N = 256 x12 2.004 vs 1.937 ms, i32 1.822 vs 1.784, N = 128 0.232 vs 0.220
+#endif
+                if constexpr (D3_STAGE_ST256 && NCK == 2) {
+                    // a run's two chunks as one 32-byte store (STG.256, §5 item 9) except the row's last run
+                    if (yr != G::NRY - 1 && d0 + e0 + EPC < p.out_width && (reinterpret_cast<unsigned long long>(rowp) & 31ull) == 0) {
+                        uint32_t v0[4], v1[4];
+                        window_chunk<E>(win, rho, 0, v0);
+                        window_chunk<E>(win, rho, 1, v1);
+                        const uint32_t v8[8] = {v0[0], v0[1], v0[2], v0[3], v1[0], v1[1], v1[2], v1[3]};
+                        st_v8(rowp, v8);
+                        goto stored;
+                    }
+                }
 #pragma unroll
                 for (int q = 0; q < NCK; ++q) {
                     uint32_t v[4];
@@ -799,6 +813,7 @@ drt_pass_kernel(const DrtPass p, const __grid_constant__ CUtensorMap omap) {
                         else *reinterpret_cast<uint4 *>(rowp + q * EPC) = make_uint4(v[0], v[1], v[2], v[3]);
                     }
                 }
+            stored:;
                 if (yr == 0 && rho > 0 && d0 >= EPC) {
                     // own elements [0, rho) end the previous chunk (whose head the previous tile wrote)
                     uint32_t tw[NWO + 4];
