@@ -128,6 +128,17 @@ template <int S> __device__ __forceinline__ int copy_row(int i) {
 // one per original axis a that z' runs along: a = 2 (z' along z): box {BW, 16, 16} over (z, y, x);
 // a = 0 / 1: box {16, 16, BW} over (z, y, x) / (z, x, y), i.e. the BW-long side outermost, so the
 // 16-byte vectors of one z' are contiguous.
+// Chunk index of item (r, lane step d) on the packing diagonal: r's 8-chunk group is kept and only the
+// position inside it rotates, so the 8 lanes of a quarter-warp write 8 distinct bank groups whether
+// or not xswz flips that group's low bit.  (NE4 not a multiple of 8: plain rotation.)
+#ifndef D3_SWAR_DIAG8
+#define D3_SWAR_DIAG8 1
+#endif
+template <int NE4> __device__ __forceinline__ int diag_chunk(int r, int d) {
+    if constexpr (D3_SWAR_DIAG8 && NE4 % 8 == 0) return (r & ~7) | ((r + d) & 7);
+    else return (r + d) % NE4;
+}
+
 struct SwarCubeMaps {
     CUtensorMap m[3];
     CUtensorMap st;       // the stage-K rows this pass writes (D3_SWAR_TMA_OUT, the copy-out)
@@ -293,7 +304,7 @@ drt_first_swar_kernel(const DrtPass p, const __grid_constant__ CUtensorMap zmap,
 #pragma unroll
                 for (int u = 0; u < NI; ++u) {
                     const int it = tid + u * G::THREADS;
-                    const int w1 = it & (S - 1), e4 = ((it / S) + w1) % NE4;
+                    const int w1 = it & (S - 1), e4 = diag_chunk<NE4>(it / S, w1);
 #pragma unroll
                     for (int t = 0; t < 4; ++t) {
                         v[u][t] = make_uint4(0u, 0u, 0u, 0u);
@@ -305,7 +316,7 @@ drt_first_swar_kernel(const DrtPass p, const __grid_constant__ CUtensorMap zmap,
                 for (int u = 0; u < NI; ++u) {
                     const int it = tid + u * G::THREADS;
                     if (it >= S * NE4) break;
-                    const int w1 = it & (S - 1), e4 = ((it / S) + w1) % NE4;
+                    const int w1 = it & (S - 1), e4 = diag_chunk<NE4>(it / S, w1);
                     uint32_t wd[4][H2];
 #pragma unroll
                     for (int t = 0; t < 4; ++t) {
@@ -324,7 +335,7 @@ drt_first_swar_kernel(const DrtPass p, const __grid_constant__ CUtensorMap zmap,
                 }
             } else {
                 // x' contiguous: one vector = all 16 w1 of (w2, z'); item (pw, e4): rows pw and pw + 8,
-                // lanes along pw with e4 on the diagonal (step 2: (pw + chunk) mod 8 = 3 pw + const)
+                // lanes along pw with e4 on the diagonal (step 2: (pw + chunk) mod 8 = 3 pw + const, diag_chunk)
                 const bool fwd = ss[0] > 0;
                 const int xoff = soff + (fwd ? 0 : 15 * ss[0]);
                 constexpr int NE4 = BW / 4, NI = (H2 * NE4 + G::THREADS - 1) / G::THREADS;
@@ -332,7 +343,7 @@ drt_first_swar_kernel(const DrtPass p, const __grid_constant__ CUtensorMap zmap,
 #pragma unroll
                 for (int u = 0; u < NI; ++u) {
                     const int it = tid + u * G::THREADS;
-                    const int pw = it & (H2 - 1), e4 = ((it / H2) + 2 * pw) % NE4;
+                    const int pw = it & (H2 - 1), e4 = diag_chunk<NE4>(it / H2, 2 * pw);
 #pragma unroll
                     for (int t = 0; t < 4; ++t) {
                         a[u][t] = make_uint4(0u, 0u, 0u, 0u);
@@ -349,7 +360,7 @@ drt_first_swar_kernel(const DrtPass p, const __grid_constant__ CUtensorMap zmap,
                 for (int u = 0; u < NI; ++u) {
                     const int it = tid + u * G::THREADS;
                     if (it >= H2 * NE4) break;
-                    const int pw = it & (H2 - 1), e4 = ((it / H2) + 2 * pw) % NE4;
+                    const int pw = it & (H2 - 1), e4 = diag_chunk<NE4>(it / H2, 2 * pw);
                     uint32_t wd[4][S];
 #pragma unroll
                     for (int t = 0; t < 4; ++t) {
