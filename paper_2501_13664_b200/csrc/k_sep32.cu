@@ -133,6 +133,35 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(THREADS, 2) drt_sep
         // consecutive coordinates 4g .. 4g + 3 of that axis, transposed in registers into 4 chunks
         const bool fy = o.fast == 1;
         const long long sf = fy ? o.sy : o.sx, so = fy ? o.sx : o.sy;
+#ifndef D3_SEP_LD256
+#define D3_SEP_LD256 1
+#endif
+        bool wide = false;
+        if constexpr (D3_SEP_LD256 && sizeof(In) == 4) wide = (reinterpret_cast<unsigned long long>(cube) & 31ull) == 0;
+        if (wide) {
+            // 32-bit voxels: one 32-byte load (LDG.256) = 8 consecutive coordinates of the unit-stride
+            // axis, half the load instructions and L1 wavefronts of the 16-byte version (every lane
+            // reads its own line here); item (other, g2, c): coordinates 8 g2 .. 8 g2 + 7 at z' = 4c .. 4c + 3
+            const int it = tid, c = it & 7;
+            const int other = fy ? (it >> 5) : (it >> 3), g2 = fy ? ((it >> 3) & 3) : 0;
+            const int f0 = fy ? 8 * g2 : 8 * k;
+            const long long base = o.off0 + (long long)(fy ? 8 * k + other : other) * so + (sf > 0 ? f0 : -(f0 + 7));
+            uint32_t v[4][8];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const In *src = cube + base + (long long)(4 * c + t) * o.sz;
+                asm volatile("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                             : "=r"(v[t][0]), "=r"(v[t][1]), "=r"(v[t][2]), "=r"(v[t][3]), "=r"(v[t][4]), "=r"(v[t][5]),
+                               "=r"(v[t][6]), "=r"(v[t][7])
+                             : "l"(src));
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int jj = sf > 0 ? j : 7 - j;
+                const int row = fy ? other * 32 + 8 * g2 + j : j * 32 + other;
+                *reinterpret_cast<uint4 *>(slab_chunk(row, c)) = make_uint4(v[0][jj], v[1][jj], v[2][jj], v[3][jj]);
+            }
+        } else
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
             const int it = tid + u * THREADS, c = it & 7;
